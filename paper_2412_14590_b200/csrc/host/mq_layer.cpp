@@ -1,0 +1,479 @@
+// mq_layer.cpp — device layer handle, the one-time packer into the engine's
+// HBM layout (mq_layout.cuh) and the forward entry points of the C ABI.
+//
+// The reference re-prepacks both sub-problems on every forward call
+// (proj/src/gemm.cpp:148-149, ~45% of its call time at M=16); here
+// packing happens once in mq_layer_create and forwards only stream weights.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../kernels/mq_kernels.hpp"
+#include "mq_internal.hpp"
+
+using namespace mq;
+
+struct mq_layer_s {
+    int device = 0;
+    int num_sms = 148;
+    int64_t N = 0, K = 0;
+    int group = 128;
+    int G = 0;
+    int64_t n8 = 0, n4 = 0;  // local (shard) rows
+    int32_t rank = 0, world = 1;
+    int64_t shard_cols = 0;
+    int w8_mode = MQ_W8_REFERENCE;
+    int64_t tiles8 = 0, tiles4 = 0;
+    uint8_t* d_wq = nullptr;
+    uint8_t* d_meta = nullptr;
+    TileDesc* d_tiles = nullptr;
+    int32_t* d_colmap = nullptr;
+    int64_t bytes_wq = 0, bytes_meta = 0, stream_bytes = 0;
+    std::vector<TileDesc> tiles;
+    std::vector<int32_t> shard_colmap;  // [world * shard_cols]
+    // internal scratch (used when the caller passes workspace = NULL)
+    std::mutex ws_mu;
+    void* d_ws = nullptr;
+    size_t ws_bytes = 0;
+};
+
+namespace {
+
+mq_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(MQ_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CU_TRY(expr)                                                  \
+    do {                                                              \
+        cudaError_t _e = (expr);                                      \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);           \
+    } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+int auto_token_tile(int64_t M) {
+    if (M <= 16) return 16;
+    if (M <= 32) return 32;
+    if (M <= 64) return 64;
+    return 128;
+}
+
+// Split-K choice for MQ_FAST: balance CTA waves against per-unit group count.
+int auto_ksplit(int64_t units1, int G, int sms) {
+    int best = 1;
+    double best_cost = 1e30;
+    for (int s = 1; s <= std::min(G, 16); ++s) {
+        const int64_t units = units1 * s;
+        const int64_t waves = (units + sms - 1) / sms;
+        const int64_t per = (G + s - 1) / s;
+        const double cost = double(waves * per) + 0.35 * (s > 1 ? 1.0 : 0.0) + 0.02 * s;
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = s;
+        }
+    }
+    return best;
+}
+
+struct Plan {
+    int bn, tb, ksplit, mode, sa_cols;
+    size_t ws_floats, counters;
+};
+
+mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
+    mq_exec_opts d{};
+    d.act_group = L->group;
+    if (!o) o = &d;
+    const int act_group = o->act_group ? o->act_group : L->group;
+    if (act_group == L->group) pl->sa_cols = L->G;
+    else if (act_group >= L->K) pl->sa_cols = 1;
+    else return fail(MQ_USAGE, "activations and weights must share group boundaries (act group " +
+                                   std::to_string(act_group) + ", weight group " + std::to_string(L->group) +
+                                   "); per-token activations use act_group = K");
+    if (o->mode != MQ_EXACT && o->mode != MQ_FAST) return fail(MQ_USAGE, "unknown mode");
+    pl->bn = o->token_tile ? o->token_tile : auto_token_tile(M);
+    if (pl->bn != 16 && pl->bn != 32 && pl->bn != 64 && pl->bn != 128)
+        return fail(MQ_USAGE, "token_tile must be 16, 32, 64 or 128");
+    pl->tb = static_cast<int>((M + pl->bn - 1) / pl->bn);
+    const int64_t tiles = L->tiles8 + L->tiles4;
+    if (o->mode == MQ_EXACT) {
+        pl->ksplit = 1;
+        pl->mode = kExactGroup;
+    } else {
+        pl->ksplit = o->ksplit ? std::min(o->ksplit, L->G) : auto_ksplit(tiles * pl->tb, L->G, L->num_sms);
+        pl->mode = pl->sa_cols == 1 ? kFastToken : kFastGroup;
+    }
+    if (pl->ksplit < 1) pl->ksplit = 1;
+    pl->ws_floats = pl->ksplit > 1 ? size_t(tiles) * pl->tb * pl->ksplit * 128 * pl->bn : 0;
+    pl->counters = pl->ksplit > 1 ? size_t(tiles) * pl->tb : 0;
+    return MQ_OK;
+}
+
+size_t plan_ws_bytes(const Plan& pl) {
+    return ((pl.counters * 4 + 255) / 256) * 256 + pl.ws_floats * 4;
+}
+
+mq_status encode_act_map(CUtensorMap* map, const int8_t* codes, int64_t ldc, int64_t M, int64_t K, int bn) {
+    auto fn = encode_fn();
+    if (!fn) return fail(MQ_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc)};
+    const cuuint32_t box[2] = {128u, static_cast<cuuint32_t>(bn)};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(codes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(MQ_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return MQ_OK;
+}
+
+mq_status check_layer(const mq_layer_s* L) {
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
+    return MQ_OK;
+}
+
+mq_status gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t M, void* Y,
+                      mq_dtype out_dtype, void* ws, GemmParams* p) {
+    std::memset(p, 0, sizeof(*p));
+    p->tiles = L->d_tiles;
+    p->num_tiles = static_cast<int32_t>(L->tiles8 + L->tiles4);
+    p->G = L->G;
+    p->K = L->K;
+    p->wq = L->d_wq;
+    p->wmeta = L->d_meta;
+    p->colmap = L->d_colmap;
+    p->sa = sa;
+    p->sa_cols = pl.sa_cols;
+    p->M = M;
+    p->Y = Y;
+    p->out_dtype = out_dtype;
+    p->ldy = L->world > 1 ? L->shard_cols : L->N;
+    p->ksplit = pl.ksplit;
+    p->token_blocks = pl.tb;
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    p->counters = reinterpret_cast<uint32_t*>(w);
+    p->ws = reinterpret_cast<float*>(w + ((pl.counters * 4 + 255) / 256) * 256);
+    p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
+    return MQ_OK;
+}
+
+mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, void** ws) {
+    if (bytes == 0) {
+        *ws = nullptr;
+        return MQ_OK;
+    }
+    std::lock_guard<std::mutex> lk(L->ws_mu);
+    if (L->ws_bytes < bytes) {
+        if (L->d_ws) cudaFree(L->d_ws);
+        L->d_ws = nullptr;
+        L->ws_bytes = 0;
+        CU_TRY(cudaMalloc(&L->d_ws, bytes));
+        CU_TRY(cudaMemset(L->d_ws, 0, bytes));
+        L->ws_bytes = bytes;
+    }
+    *ws = L->d_ws;
+    return MQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int device, mq_layer_t* out) {
+    if (!out) return fail(MQ_USAGE, "out handle is null");
+    if (mq_status st = validate_desc(d)) return st;
+    if (d->group_size != kGroupK)
+        return fail(MQ_USAGE, "group size " + std::to_string(d->group_size) +
+                                  " not supported by the sm_100a engine (tcgen05 tiles use group 128, the reference default)");
+    mq_layer_opts o{MQ_W8_REFERENCE, 0, 1};
+    if (opts) o = *opts;
+    if (o.world < 1 || o.rank < 0 || o.rank >= o.world) return fail(MQ_USAGE, "bad rank/world");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(MQ_CUDA, "no CUDA device: the engine has no CPU fallback");
+    if (device < 0 || device >= ndev) return fail(MQ_USAGE, "bad device ordinal");
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    if (major != 10) return fail(MQ_CUDA, "the engine is built for sm_100a (B200); device is sm_" + std::to_string(major) + "x");
+    CU_TRY(cudaSetDevice(device));
+
+    auto* L = new mq_layer_s;
+    L->device = device;
+    cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, device);
+    L->N = d->out_features;
+    L->K = d->in_features;
+    L->group = d->group_size;
+    L->G = static_cast<int>(num_groups(L->K, L->group));
+    L->rank = o.rank;
+    L->world = o.world;
+    L->w8_mode = o.w8_mode;
+    const int64_t K = L->K, G = L->G;
+
+    // Shard: rank r owns rows [r*n/W, (r+1)*n/W) of each sub-problem.
+    auto lo = [&](int64_t n, int r) { return n * r / o.world; };
+    const int64_t a8 = lo(d->n8, o.rank), b8 = lo(d->n8, o.rank + 1);
+    const int64_t a4 = lo(d->n4, o.rank), b4 = lo(d->n4, o.rank + 1);
+    L->n8 = b8 - a8;
+    L->n4 = b4 - a4;
+    L->tiles8 = (L->n8 + kTileRows - 1) / kTileRows;
+    L->tiles4 = (L->n4 + kTileRows - 1) / kTileRows;
+    if (o.world > 1) {
+        int64_t sc = 0;
+        for (int r = 0; r < o.world; ++r)
+            sc = std::max(sc, (lo(d->n8, r + 1) - lo(d->n8, r)) + (lo(d->n4, r + 1) - lo(d->n4, r)));
+        L->shard_cols = sc;
+        L->shard_colmap.assign(size_t(o.world * sc), -1);
+        for (int r = 0; r < o.world; ++r) {
+            int64_t j = 0;
+            for (int64_t i = lo(d->n8, r); i < lo(d->n8, r + 1); ++i) L->shard_colmap[r * sc + j++] = d->index_map8[i];
+            for (int64_t i = lo(d->n4, r); i < lo(d->n4, r + 1); ++i) L->shard_colmap[r * sc + j++] = d->index_map4[i];
+        }
+    } else {
+        L->shard_cols = L->N;
+    }
+
+    // ---- pack (host), then upload once
+    const int64_t T = L->tiles8 + L->tiles4;
+    L->bytes_wq = (L->tiles8 * kCodes8Bytes + L->tiles4 * kCodes4Bytes) * G;
+    L->bytes_meta = (L->tiles8 * kMeta8Bytes + L->tiles4 * kMeta4Bytes) * G;
+    std::vector<uint8_t> wq(size_t(std::max<int64_t>(L->bytes_wq, 1)), 0);
+    std::vector<uint8_t> meta(size_t(std::max<int64_t>(L->bytes_meta, 1)), 0);
+    std::vector<int32_t> colmap(size_t(std::max<int64_t>(T * kTileRows, 1)), -1);
+    L->tiles.resize(size_t(T));
+    int64_t coff = 0, moff = 0;
+    const int64_t stride4 = row_stride(4, K);
+    for (int64_t t = 0; t < T; ++t) {
+        const bool is8 = t < L->tiles8;
+        const int64_t first = is8 ? t * kTileRows : (t - L->tiles8) * kTileRows;  // local sub row
+        const int64_t nloc = is8 ? L->n8 : L->n4;
+        const int rows = static_cast<int>(std::min<int64_t>(kTileRows, nloc - first));
+        TileDesc& td = L->tiles[t];
+        td.codes_off = coff;
+        td.meta_off = moff;
+        td.is8 = is8;
+        td.rows = rows;
+        td.colmap_off = static_cast<int32_t>(t * kTileRows);
+        td.copy_bytes = is8 ? ((rows + 7) / 8) * 1024 : rows * 64;
+        td.sub_row0 = static_cast<int32_t>(first);
+        td.pad = 0;
+        for (int r = 0; r < rows; ++r) {
+            const int64_t srow = (is8 ? a8 : a4) + first + r;  // global sub-problem row
+            const int64_t lcol = (is8 ? 0 : L->n8) + first + r;  // local gather column
+            colmap[t * kTileRows + r] = o.world > 1 ? static_cast<int32_t>(lcol)
+                                                    : (is8 ? d->index_map8[srow] : d->index_map4[srow]);
+        }
+        for (int64_t g = 0; g < G; ++g) {
+            const int64_t k0 = g * kGroupK;
+            uint8_t* cb = wq.data() + coff + g * (is8 ? kCodes8Bytes : kCodes4Bytes);
+            uint8_t* mb = meta.data() + moff + g * (is8 ? kMeta8Bytes : kMeta4Bytes);
+            for (int r = 0; r < rows; ++r) {
+                const int64_t srow = (is8 ? a8 : a4) + first + r;
+                float sc;
+                if (is8) {
+                    const uint8_t* src = d->payload8 + srow * K;
+                    for (int k = 0; k < kGroupK && k0 + k < K; ++k) cb[sw128_offset(r, k)] = src[k0 + k];
+                    sc = d->scales8[srow * G + g];
+                } else {
+                    const uint8_t* src = d->payload4 + srow * stride4;
+                    for (int ch = 0; ch < 8; ++ch) {
+                        uint8_t e[16];
+                        for (int j = 0; j < 16; ++j) {
+                            const int64_t k = k0 + ch * 16 + j;
+                            e[j] = k < K ? ((k & 1) ? (src[k / 2] >> 4) : (src[k / 2] & 0x0F)) : 0;
+                        }
+                        uint32_t w0, w1;
+                        pack_chunk4(e, &w0, &w1);
+                        std::memcpy(cb + r * 64 + ch * 8, &w0, 4);
+                        std::memcpy(cb + r * 64 + ch * 8 + 4, &w1, 4);
+                    }
+                    sc = d->scales4[srow * G + g];
+                    mb[512 + r] = d->zero_points4[srow * G + g];
+                }
+                std::memcpy(mb + 4 * r, &sc, 4);
+            }
+        }
+        coff += (is8 ? kCodes8Bytes : kCodes4Bytes) * G;
+        moff += (is8 ? kMeta8Bytes : kMeta4Bytes) * G;
+        L->stream_bytes += int64_t(td.copy_bytes + (is8 ? kMeta8Bytes : kMeta4Bytes)) * G;
+    }
+
+    auto upload = [&](void** dst, const void* src, size_t n) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, std::max<size_t>(n, 16));
+        if (e != cudaSuccess) return e;
+        return n ? cudaMemcpy(*dst, src, n, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    cudaError_t e = upload(reinterpret_cast<void**>(&L->d_wq), wq.data(), size_t(L->bytes_wq));
+    if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_meta), meta.data(), size_t(L->bytes_meta));
+    if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_tiles), L->tiles.data(), L->tiles.size() * sizeof(TileDesc));
+    if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_colmap), colmap.data(), colmap.size() * 4);
+    if (e != cudaSuccess) {
+        mq_layer_destroy(L);
+        return cuda_fail(e, "layer upload");
+    }
+    *out = L;
+    return MQ_OK;
+}
+
+void mq_layer_destroy(mq_layer_t L) {
+    if (!L) return;
+    cudaFree(L->d_wq);
+    cudaFree(L->d_meta);
+    cudaFree(L->d_tiles);
+    cudaFree(L->d_colmap);
+    if (L->d_ws) cudaFree(L->d_ws);
+    delete L;
+}
+
+mq_status mq_layer_get_info(mq_layer_t L, mq_layer_info* info) {
+    if (mq_status st = check_layer(L)) return st;
+    info->out_features = L->N;
+    info->in_features = L->K;
+    info->group_size = L->group;
+    info->n8 = L->n8;
+    info->n4 = L->n4;
+    info->tiles8 = L->tiles8;
+    info->tiles4 = L->tiles4;
+    info->device_bytes = L->bytes_wq + L->bytes_meta;
+    info->weight_stream_bytes = L->stream_bytes;
+    info->rank = L->rank;
+    info->world = L->world;
+    info->shard_cols = L->shard_cols;
+    return MQ_OK;
+}
+
+mq_status mq_layer_shard_colmap(mq_layer_t L, int32_t* out) {
+    if (mq_status st = check_layer(L)) return st;
+    if (L->world == 1) return fail(MQ_USAGE, "layer is not sharded");
+    std::copy(L->shard_colmap.begin(), L->shard_colmap.end(), out);
+    return MQ_OK;
+}
+
+mq_status mq_quantize_act(const void* A, mq_dtype dt, int64_t M, int64_t K, int64_t lda, int32_t group,
+                          int8_t* codes, int64_t ldc, float* scales, int32_t* err, void* stream) {
+    if (M < 0 || K < 1) return fail(MQ_USAGE, "bad activation shape");
+    if (group < 1) return fail(MQ_USAGE, "group_size must be >= 1");
+    if (lda < K || ldc < K) return fail(MQ_USAGE, "leading dimension smaller than K");
+    if (dt != MQ_F32 && dt != MQ_F16 && dt != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
+    cudaError_t e = launch_act_quant(A, dt, M, K, lda, group >= K ? int(K) : group, 0, codes, ldc, scales, err,
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
+    return MQ_OK;
+}
+
+size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
+    Plan pl;
+    if (!L || make_plan(L, M, o, &pl) != MQ_OK) return 0;
+    return plan_ws_bytes(pl);
+}
+
+mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, const float* scales, int64_t M,
+                                void* Y, mq_dtype out_dtype, const mq_exec_opts* o, void* ws, void* stream) {
+    if (mq_status st = check_layer(L)) return st;
+    if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
+    if (M == 0) return MQ_OK;
+    if (ldc < L->K || ldc % 16 != 0) return fail(MQ_USAGE, "ldc must be >= K and a multiple of 16 (TMA row pitch)");
+    if (reinterpret_cast<uintptr_t>(codes) % 16 != 0) return fail(MQ_USAGE, "codes must be 16-byte aligned");
+    if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
+    Plan pl;
+    if (mq_status st = make_plan(L, M, o, &pl)) return st;
+    if (!ws) {
+        if (mq_status st = ensure_internal_ws(L, plan_ws_bytes(pl), &ws)) return st;
+    }
+    GemmParams p;
+    gemm_params(L, pl, scales, M, Y, out_dtype, ws, &p);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    if (o && o->gemm_impl == 1) {
+        e = launch_mixed_gemm_simt(p, codes, ldc, pl.mode == kFastToken ? kFastToken : kExactGroup,
+                                   L->w8_mode == MQ_W8_REFERENCE, s);
+    } else {
+        alignas(64) CUtensorMap map;
+        if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
+        e = launch_mixed_gemm_tc(p, &map, pl.bn, pl.mode, L->num_sms, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
+    return MQ_OK;
+}
+
+size_t mq_mixed_linear_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
+    if (!L) return 0;
+    const int64_t ldc = (L->K + 127) / 128 * 128;
+    const int act_group = (o && o->act_group) ? o->act_group : L->group;
+    const int64_t sa_cols = act_group >= L->K ? 1 : L->G;
+    const size_t head = size_t((M * ldc + 255) / 256 * 256) + size_t((M * sa_cols * 4 + 255) / 256 * 256);
+    return head + mq_forward_workspace_bytes(L, M, o);
+}
+
+mq_status mq_mixed_linear(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t M, void* Y, mq_dtype out_dtype,
+                          const mq_exec_opts* o, void* ws, int32_t* err, void* stream) {
+    if (mq_status st = check_layer(L)) return st;
+    if (M == 0) return MQ_OK;
+    mq_exec_opts d{};
+    if (!o) o = &d;
+    const int act_group = o->act_group ? o->act_group : L->group;
+    Plan pl;
+    if (mq_status st = make_plan(L, M, o, &pl)) return st;
+    const int64_t ldc = (L->K + 127) / 128 * 128;
+    const size_t need = mq_mixed_linear_workspace_bytes(L, M, o);
+    if (!ws) {
+        if (mq_status st = ensure_internal_ws(L, need, &ws)) return st;
+    }
+    uint8_t* w = static_cast<uint8_t*>(ws);
+    int8_t* codes = reinterpret_cast<int8_t*>(w);
+    const int64_t sa_cols = pl.sa_cols;
+    float* scales = reinterpret_cast<float*>(w + (M * ldc + 255) / 256 * 256);
+    void* gws = w + (M * ldc + 255) / 256 * 256 + (M * sa_cols * 4 + 255) / 256 * 256;
+    if (mq_status st = mq_quantize_act(A, a_dtype, M, L->K, L->K, act_group >= L->K ? int32_t(L->K) : act_group,
+                                       codes, ldc, scales, err, stream))
+        return st;
+    return mq_mixed_linear_codes(L, codes, ldc, scales, M, Y, out_dtype, o, gws, stream);
+}
+
+mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64_t M, int32_t which,
+                           int32_t* partials, void* stream) {
+    if (mq_status st = check_layer(L)) return st;
+    if (which != 0 && which != 1) return fail(MQ_USAGE, "which must be 0 (sub8) or 1 (sub4)");
+    if (ldc < L->K || ldc % 16 != 0) return fail(MQ_USAGE, "ldc must be >= K and a multiple of 16");
+    if (M == 0) return MQ_OK;
+    Plan pl;
+    if (mq_status st = make_plan(L, M, nullptr, &pl)) return st;
+    GemmParams p;
+    gemm_params(L, pl, nullptr, M, nullptr, MQ_F32, nullptr, &p);
+    p.tiles = L->d_tiles + (which == 0 ? 0 : L->tiles8);
+    p.num_tiles = static_cast<int32_t>(which == 0 ? L->tiles8 : L->tiles4);
+    if (p.num_tiles == 0) return MQ_OK;
+    p.ksplit = 1;
+    p.partials = partials;
+    p.partial_rows = static_cast<int32_t>(which == 0 ? L->n8 : L->n4);
+    alignas(64) CUtensorMap map;
+    if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
+    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, kDumpPartials, L->num_sms, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "partials launch");
+    return MQ_OK;
+}
+
+mq_status mq_permute_gathered(const void* gathered, const int32_t* colmap, int32_t world, int64_t sc, int64_t M,
+                              int64_t N, void* Y, mq_dtype dt, void* stream) {
+    if (world < 1 || sc < 0 || M < 0) return fail(MQ_USAGE, "bad permute shape");
+    cudaError_t e = launch_permute(gathered, colmap, world, sc, M, N, Y, dt, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "permute launch");
+    return MQ_OK;
+}
+
+}  // extern "C"

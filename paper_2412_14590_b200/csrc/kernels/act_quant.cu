@@ -1,0 +1,144 @@
+// act_quant.cu — K1: dynamic symmetric int8 activation quantization.
+//
+// Restates quantize_group_sym<float> (proj/include/mixquant/quant.hpp:117-140)
+// as called by execute_mixed_linear (proj/src/gemm.cpp:190), bit for bit:
+//   amax = max|x| (f32), s = amax == 0 ? 1e-8f : amax / 127.0f (IEEE division),
+//   s == 0 -> max(amax, 1e-8f), optional f16 rounding (quant.cpp:81-86),
+//   code = clamp(roundf(x / s), -127, 127) with IEEE division and
+//   round-half-away-from-zero. Non-finite input sets *err to the smallest
+//   flat group index m*G+g (the reference throws DataError, quant.hpp:56-64).
+// Two launch shapes: a warp per (token, group) for the group-wise parity mode,
+// a CTA per token for the per-token mode (group == K). HBM-bound: each element
+// is read once (f32/f16/bf16) and written once as int8.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <climits>
+
+#include "mq_kernels.hpp"
+
+namespace mq {
+namespace {
+
+template <int DT>
+__device__ __forceinline__ float load_act(const void* A, int64_t i) {
+    if constexpr (DT == 0) return __ldg(static_cast<const float*>(A) + i);
+    else if constexpr (DT == 1) return __half2float(static_cast<const __half*>(A)[i]);
+    else return __bfloat162float(static_cast<const __nv_bfloat16*>(A)[i]);
+}
+
+__device__ __forceinline__ float act_scale(float amax, int f16) {
+    float s = (amax == 0.0f) ? 1e-8f : __fdiv_rn(amax, 127.0f);
+    if (s == 0.0f) s = fmaxf(amax, 1e-8f);
+    if (f16) {
+        s = __half2float(__float2half_rn(s));
+        if (!(s > 0.0f)) s = 5.9604644775390625e-8f;
+    }
+    return s;
+}
+
+__device__ __forceinline__ int8_t quant_one(float x, float s) {
+    float q = roundf(__fdiv_rn(x, s));
+    q = fminf(fmaxf(q, -127.0f), 127.0f);
+    return static_cast<int8_t>(static_cast<int>(q));
+}
+
+// One warp per (token m, group g); group <= 4096.
+template <int DT>
+__global__ void act_quant_group_kernel(const void* __restrict__ A, int64_t M, int64_t K,
+                                       int64_t lda, int group, int G, int f16,
+                                       int8_t* __restrict__ codes, int64_t ldc,
+                                       float* __restrict__ scales, int32_t* err) {
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= M * G) return;
+    const int64_t m = wid / G;
+    const int g = static_cast<int>(wid - m * G);
+    const int64_t b = int64_t(g) * group;
+    const int len = static_cast<int>(K - b < group ? K - b : int64_t(group));
+    const int64_t base = m * lda + b;
+
+    float amax = 0.0f;
+    bool finite = true;
+    for (int i = lane; i < len; i += 32) {
+        const float x = load_act<DT>(A, base + i);
+        finite &= isfinite(x);
+        amax = fmaxf(amax, fabsf(x));
+    }
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    finite = __all_sync(0xffffffffu, finite);
+    if (!finite && lane == 0 && err) atomicMin(err, static_cast<int32_t>(wid));
+    const float s = act_scale(amax, f16);
+    int8_t* crow = codes + m * ldc + b;
+    for (int i = lane; i < len; i += 32) crow[i] = quant_one(load_act<DT>(A, base + i), s);
+    if (lane == 0) scales[m * G + g] = s;
+    // zero the padding columns [K, ldc) once per row (owned by the last group)
+    if (g == G - 1)
+        for (int64_t c = K + lane; c < ldc; c += 32) codes[m * ldc + c] = 0;
+}
+
+// One CTA per token (per-token mode, group == K).
+template <int DT>
+__global__ void __launch_bounds__(256) act_quant_row_kernel(
+    const void* __restrict__ A, int64_t K, int64_t lda, int f16, int8_t* __restrict__ codes,
+    int64_t ldc, float* __restrict__ scales, int32_t* err) {
+    __shared__ float red[8];
+    __shared__ int bad[8];
+    const int64_t m = blockIdx.x;
+    const int64_t base = m * lda;
+    float amax = 0.0f;
+    bool finite = true;
+    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+        const float x = load_act<DT>(A, base + i);
+        finite &= isfinite(x);
+        amax = fmaxf(amax, fabsf(x));
+    }
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const bool wfin = __all_sync(0xffffffffu, finite);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[w] = amax;
+        bad[w] = !wfin;
+    }
+    __syncthreads();
+    amax = red[0];
+    int anybad = bad[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+        amax = fmaxf(amax, red[i]);
+        anybad |= bad[i];
+    }
+    if (anybad && threadIdx.x == 0 && err) atomicMin(err, static_cast<int32_t>(m));
+    const float s = act_scale(amax, f16);
+    for (int64_t i = threadIdx.x; i < K; i += blockDim.x)
+        codes[m * ldc + i] = quant_one(load_act<DT>(A, base + i), s);
+    for (int64_t c = K + threadIdx.x; c < ldc; c += blockDim.x) codes[m * ldc + c] = 0;
+    if (threadIdx.x == 0) scales[m] = s;
+}
+
+}  // namespace
+
+cudaError_t launch_act_quant(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda,
+                             int group, int f16, int8_t* codes, int64_t ldc, float* scales,
+                             int32_t* err, cudaStream_t stream) {
+    if (M == 0) return cudaSuccess;
+    if (group >= K) {
+        const dim3 grid(static_cast<unsigned>(M));
+        switch (a_dtype) {
+            case 0: act_quant_row_kernel<0><<<grid, 256, 0, stream>>>(A, K, lda, f16, codes, ldc, scales, err); break;
+            case 1: act_quant_row_kernel<1><<<grid, 256, 0, stream>>>(A, K, lda, f16, codes, ldc, scales, err); break;
+            default: act_quant_row_kernel<2><<<grid, 256, 0, stream>>>(A, K, lda, f16, codes, ldc, scales, err); break;
+        }
+    } else {
+        const int G = static_cast<int>((K + group - 1) / group);
+        const int64_t warps = M * G;
+        const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));
+        switch (a_dtype) {
+            case 0: act_quant_group_kernel<0><<<grid, 256, 0, stream>>>(A, M, K, lda, group, G, f16, codes, ldc, scales, err); break;
+            case 1: act_quant_group_kernel<1><<<grid, 256, 0, stream>>>(A, M, K, lda, group, G, f16, codes, ldc, scales, err); break;
+            default: act_quant_group_kernel<2><<<grid, 256, 0, stream>>>(A, M, K, lda, group, G, f16, codes, ldc, scales, err); break;
+        }
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace mq

@@ -1,0 +1,383 @@
+"""Python mirror of the reference's `mixquant` hot-path API over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(proj/include/mixquant/{quant,mixed,gemm}.hpp): UsageError / DataError are
+raised before any compute. Host packing runs in the C++ library (bit-exact);
+every GEMM runs on the B200 through libmixllm_b200.so — there is no CPU path.
+Device buffers are torch CUDA tensors (plumbing only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import capi
+from .capi import DataError, UsageError, check, lib  # noqa: F401
+
+P = C.c_void_p
+
+
+def _p(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(P)
+    return C.c_void_p(a.data_ptr())  # torch tensor
+
+
+# ------------------------------------------------------------------ schemes
+@dataclass(frozen=True)
+class QuantScheme:
+    """QuantScheme (quant.hpp:25-36)."""
+    bit_width: int = 4
+    symmetric: bool = False
+    group_size: int = 128
+    scale_f16_storage: bool = False
+
+    def c(self) -> capi.mq_scheme:
+        return capi.mq_scheme(self.bit_width, int(self.symmetric), self.group_size, int(self.scale_f16_storage))
+
+
+LARGEBIT = QuantScheme(8, True, 128)   # gemm.cpp:229
+SMALLBIT = QuantScheme(4, False, 128)  # gemm.cpp:230
+ACT_SCHEME = QuantScheme(8, True, 128)  # gemm.cpp:231
+
+
+@dataclass
+class QuantizedTensor:
+    """QuantizedTensor (quant.hpp:146-176), reference layouts, host numpy."""
+    scheme: QuantScheme
+    rows: int
+    cols: int
+    payload: np.ndarray
+    scales: np.ndarray
+    zero_points: np.ndarray | None
+
+    def num_groups(self) -> int:
+        return 0 if self.cols == 0 else (self.cols + self.scheme.group_size - 1) // self.scheme.group_size
+
+    def row_stride_bytes(self) -> int:
+        return (self.cols + 1) // 2 if self.scheme.bit_width == 4 else self.cols
+
+    def code(self, r: int, c: int) -> int:
+        if self.scheme.bit_width == 4:
+            b = int(self.payload[r, c // 2])
+            return (b >> 4) if c % 2 else (b & 0x0F)
+        b = int(self.payload[r, c])
+        return b - 256 if (self.scheme.symmetric and b > 127) else b
+
+
+def quantize_tensor(m: np.ndarray, scheme: QuantScheme) -> QuantizedTensor:
+    """quantize_tensor<float|double> (quant.hpp:183-243)."""
+    m = np.ascontiguousarray(m)
+    if m.ndim != 2:
+        raise UsageError("quantize_tensor expects a matrix")
+    rows, cols = m.shape
+    g = scheme.group_size
+    if g < 1:
+        raise UsageError(f"group_size must be >= 1, got {g}")
+    G = 0 if cols == 0 else (cols + g - 1) // g
+    stride = (cols + 1) // 2 if scheme.bit_width == 4 else cols
+    payload = np.zeros((rows, stride), np.uint8)
+    scales = np.zeros((rows, G), np.float32)
+    zps = None if scheme.symmetric else np.zeros((rows, G), np.uint8)
+    sc = scheme.c()
+    if m.dtype == np.float64:
+        st = lib().mq_quantize_tensor_f64(_p(m), rows, cols, C.byref(sc), _p(payload), _p(scales), _p(zps), None, None)
+    elif m.dtype == np.float32:
+        st = lib().mq_quantize_tensor_f32(_p(m), rows, cols, C.byref(sc), _p(payload), _p(scales), _p(zps), None, None)
+    else:
+        raise UsageError(f"unsupported dtype {m.dtype}")
+    check(st)
+    return QuantizedTensor(scheme, rows, cols, payload, scales, zps)
+
+
+def pack_nibbles(values) -> np.ndarray:
+    v = np.ascontiguousarray(np.asarray(values, np.uint8))
+    out = np.zeros((v.size + 1) // 2, np.uint8)
+    check(lib().mq_pack_nibbles(_p(v), v.size, _p(out)))
+    return out
+
+
+def unpack_nibbles(data, count: int) -> np.ndarray:
+    b = np.ascontiguousarray(np.asarray(data, np.uint8))
+    out = np.zeros(max(count, 0), np.uint8)
+    check(lib().mq_unpack_nibbles(_p(b), b.size, count, _p(out)))
+    return out
+
+
+def fast_i2f(x: int) -> float:
+    return lib().mq_fast_i2f(x)
+
+
+def round_scale_f16(s: float) -> float:
+    return lib().mq_round_scale_f16(s)
+
+
+def fnv1a_hex(a) -> str:
+    a = np.ascontiguousarray(a)
+    return "%016x" % lib().mq_fnv1a(_p(a), a.nbytes)
+
+
+# ----------------------------------------------------------------- layers
+@dataclass
+class MixedLinearLayer:
+    """MixedLinearLayer (mixed.hpp:16-24): reference layouts on the host."""
+    name: str
+    out_features: int
+    in_features: int
+    sub8: QuantizedTensor
+    sub4: QuantizedTensor
+    index_map8: np.ndarray
+    index_map4: np.ndarray
+    _keep: list = field(default_factory=list, repr=False)
+
+    def desc(self) -> capi.mq_layer_desc:
+        d = capi.mq_layer_desc()
+        d.out_features = self.out_features
+        d.in_features = self.in_features
+        d.group_size = (self.sub4 if self.sub4.rows else self.sub8).scheme.group_size
+        d.n8, d.n4 = self.sub8.rows, self.sub4.rows
+        arrs = [np.ascontiguousarray(x) for x in (self.index_map8.astype(np.int32), self.index_map4.astype(np.int32),
+                                                  self.sub8.payload, self.sub8.scales, self.sub4.payload,
+                                                  self.sub4.scales,
+                                                  self.sub4.zero_points if self.sub4.zero_points is not None
+                                                  else np.zeros((0,), np.uint8))]
+        self._keep = arrs
+        (d.index_map8, d.index_map4, d.payload8, d.scales8, d.payload4, d.scales4, d.zero_points4) = \
+            [a.ctypes.data for a in arrs]
+        return d
+
+
+def partition_and_quantize(weight: np.ndarray, promoted, largebit: QuantScheme = LARGEBIT,
+                           smallbit: QuantScheme = SMALLBIT, name: str = "") -> MixedLinearLayer:
+    """partition_and_quantize (mixed.cpp:46-81) — host C++, bit-exact."""
+    W = np.ascontiguousarray(weight, np.float64)
+    N, K = W.shape
+    prom = np.ascontiguousarray(np.asarray(promoted, np.int32).reshape(-1))
+    h = C.c_void_p()
+    check(lib().mq_partition_and_quantize(_p(W), N, K, _p(prom), prom.size, C.byref(largebit.c()),
+                                          C.byref(smallbit.c()), C.byref(h)))
+    try:
+        d = capi.mq_layer_desc()
+        check(lib().mq_host_layer_desc(h, C.byref(d)))
+        G = 0 if K == 0 else (K + largebit.group_size - 1) // largebit.group_size
+
+        def arr(ptr, n, dt):
+            if n == 0:
+                return np.zeros((0,), dt)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), (n,)).copy()
+
+        n8, n4 = d.n8, d.n4
+        sub8 = QuantizedTensor(largebit, n8, K, arr(d.payload8, n8 * K, np.uint8).reshape(n8, K),
+                               arr(d.scales8, n8 * G, np.float32).reshape(n8, G), None)
+        s4 = (K + 1) // 2
+        sub4 = QuantizedTensor(smallbit, n4, K, arr(d.payload4, n4 * s4, np.uint8).reshape(n4, s4),
+                               arr(d.scales4, n4 * G, np.float32).reshape(n4, G),
+                               arr(d.zero_points4, n4 * G, np.uint8).reshape(n4, G))
+        return MixedLinearLayer(name, N, K, sub8, sub4, arr(d.index_map8, n8, np.int32), arr(d.index_map4, n4, np.int32))
+    finally:
+        lib().mq_host_layer_destroy(h)
+
+
+def validate_mixed_layer(layer: MixedLinearLayer) -> None:
+    check(lib().mq_validate_layer(C.byref(layer.desc())))
+
+
+def prepack_weights(layer: MixedLinearLayer, which: int) -> np.ndarray:
+    """prepack_weights (gemm.cpp:89-108) of sub8 (which=0) / sub4 (which=1)."""
+    rows = layer.sub8.rows if which == 0 else layer.sub4.rows
+    out = np.zeros(rows * layer.in_features, np.uint8)
+    check(lib().mq_prepack_reference(C.byref(layer.desc()), which, _p(out)))
+    return out
+
+
+def reassemble_output(y8, y4, map8, map4, out_features: int) -> np.ndarray:
+    """reassemble_output (mixed.cpp:83-120) on host arrays."""
+    y8 = np.ascontiguousarray(y8, np.float32)
+    y4 = np.ascontiguousarray(y4, np.float32)
+    map8 = np.ascontiguousarray(map8, np.int32)
+    map4 = np.ascontiguousarray(map4, np.int32)
+    if y8.shape[1] != map8.size or y4.shape[1] != map4.size:
+        raise UsageError("reassemble_output: column counts do not match index maps")
+    M = max(y8.shape[0], y4.shape[0])
+    out = np.zeros((M, out_features), np.float32)
+    check(lib().mq_reassemble_output(_p(y8), map8.size, _p(y4), map4.size, _p(map8), _p(map4), M, out_features,
+                                     _p(out)))
+    return out
+
+
+def bench_inputs(m: int, n: int, k: int, percent: float, seed: int = 1):
+    """run_bench's synthetic inputs (gemm.cpp:211-227), byte-for-byte."""
+    W = np.empty((n, k), np.float64)
+    A = np.empty((m, k), np.float32)
+    prom = np.empty(max(n, 1), np.int32)
+    cnt = lib().mq_bench_inputs(m, n, k, percent, seed, _p(W), _p(A), _p(prom))
+    return W, A, prom[:cnt].copy()
+
+
+# ------------------------------------------------------------ device engine
+_DT = {"float32": capi.MQ_F32, "float16": capi.MQ_F16, "bfloat16": capi.MQ_BF16}
+
+
+def _dt(t) -> int:
+    return _DT[str(t.dtype).replace("torch.", "")]
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def exec_opts(mode: int = capi.MQ_EXACT, act_group: int = 0, ksplit: int = 0, token_tile: int = 0,
+              gemm_impl: int = 0) -> capi.mq_exec_opts:
+    return capi.mq_exec_opts(mode, act_group, ksplit, token_tile, gemm_impl)
+
+
+class DeviceLayer:
+    """A mixed layer packed once into the engine's HBM layout (mq_layer_create)."""
+
+    def __init__(self, layer: MixedLinearLayer, device: int = 0, w8_mode: int = capi.MQ_W8_REFERENCE,
+                 rank: int = 0, world: int = 1):
+        self.layer = layer
+        opts = capi.mq_layer_opts(w8_mode, rank, world)
+        h = C.c_void_p()
+        check(lib().mq_layer_create(C.byref(layer.desc()), C.byref(opts), device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self.info = capi.mq_layer_info()
+        check(lib().mq_layer_get_info(h, C.byref(self.info)))
+        self._ws = {}
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().mq_layer_destroy(h)
+            self.h = None
+
+    @property
+    def out_cols(self) -> int:
+        return self.info.shard_cols if self.info.world > 1 else self.info.out_features
+
+    def shard_colmap(self) -> np.ndarray:
+        out = np.zeros(self.info.world * self.info.shard_cols, np.int32)
+        check(lib().mq_layer_shard_colmap(self.h, _p(out)))
+        return out
+
+    def workspace(self, M: int, opts: capi.mq_exec_opts, full: bool = True):
+        import torch
+        n = (lib().mq_mixed_linear_workspace_bytes if full else lib().mq_forward_workspace_bytes)(
+            self.h, M, C.byref(opts))
+        key = (full, n)
+        if key not in self._ws:
+            self._ws[key] = torch.zeros(max(int(n), 16), dtype=torch.uint8, device=f"cuda:{self.device}")
+        return self._ws[key]
+
+    def forward(self, A, out=None, out_dtype=None, opts: capi.mq_exec_opts | None = None, err=None,
+                stream=None, workspace=None):
+        """execute_mixed_linear on device: A [M, K] f32/f16/bf16 (torch cuda)."""
+        import torch
+        opts = opts or exec_opts()
+        M = A.shape[0]
+        if out is None:
+            out = torch.empty((M, self.out_cols), dtype=out_dtype or torch.float32, device=A.device)
+        ws = workspace if workspace is not None else self.workspace(M, opts, True)
+        check(lib().mq_mixed_linear(self.h, _p(A), _dt(A), M, _p(out), _dt(out), C.byref(opts), _p(ws),
+                                    _p(err), _stream(stream)))
+        return out
+
+    def forward_codes(self, codes, scales, out=None, out_dtype=None, opts: capi.mq_exec_opts | None = None,
+                      stream=None, workspace=None):
+        """execute_mixed_on_codes on device: codes int8 [M, ldc], scales f32."""
+        import torch
+        opts = opts or exec_opts()
+        M = codes.shape[0]
+        if out is None:
+            out = torch.empty((M, self.out_cols), dtype=out_dtype or torch.float32, device=codes.device)
+        ws = workspace if workspace is not None else self.workspace(M, opts, False)
+        check(lib().mq_mixed_linear_codes(self.h, _p(codes), codes.stride(0), _p(scales), M, _p(out), _dt(out),
+                                          C.byref(opts), _p(ws), _stream(stream)))
+        return out
+
+    def partials(self, codes, which: int, stream=None):
+        import torch
+        M = codes.shape[0]
+        rows = self.info.n8 if which == 0 else self.info.n4
+        G = (self.info.in_features + self.info.group_size - 1) // self.info.group_size
+        out = torch.zeros((G, M, rows), dtype=torch.int32, device=codes.device)
+        check(lib().mq_gemm_partials(self.h, _p(codes), codes.stride(0), M, which, _p(out), _stream(stream)))
+        return out
+
+
+def quantize_act(A, group_size: int, ldc: int | None = None, err=None, stream=None):
+    """Activation quantization on device: returns (codes int8 [M, ldc], scales f32)."""
+    import torch
+    M, K = A.shape
+    ldc = ldc or (K + 127) // 128 * 128
+    codes = torch.empty((M, ldc), dtype=torch.int8, device=A.device)
+    G = 1 if group_size >= K else (K + group_size - 1) // group_size
+    scales = torch.empty((M, G), dtype=torch.float32, device=A.device)
+    check(lib().mq_quantize_act(_p(A), _dt(A), M, K, A.stride(0), group_size, _p(codes), ldc, _p(scales), _p(err),
+                                _stream(stream)))
+    return codes, scales
+
+
+def permute_gathered(gathered, colmap_dev, world: int, shard_cols: int, M: int, N: int, out=None, stream=None):
+    import torch
+    if out is None:
+        out = torch.empty((M, N), dtype=gathered.dtype, device=gathered.device)
+    check(lib().mq_permute_gathered(_p(gathered), _p(colmap_dev), world, shard_cols, M, N, _p(out), _dt(out),
+                                    _stream(stream)))
+    return out
+
+
+# ----------------------------------------------- reference-shaped drop-ins
+def execute_mixed_linear(activations: np.ndarray, layer: MixedLinearLayer, act_scheme: QuantScheme = ACT_SCHEME,
+                         mode: int = capi.MQ_EXACT, w8_mode: int = capi.MQ_W8_REFERENCE,
+                         device: int = 0) -> np.ndarray:
+    """execute_mixed_linear (gemm.cpp:183-192): host f32 in, host f32 out,
+    computed on the B200 (synchronous, like the reference)."""
+    import torch
+    if act_scheme.bit_width != 8 or not act_scheme.symmetric:
+        raise UsageError("activation scheme must be 8-bit symmetric")
+    A = np.ascontiguousarray(activations, np.float32)
+    if A.shape[1] != layer.in_features:
+        raise UsageError("activation K does not match the layer's in_features")
+    dl = DeviceLayer(layer, device, w8_mode)
+    err = torch.full((1,), 2**31 - 1, dtype=torch.int32, device=f"cuda:{device}")
+    Y = dl.forward(torch.from_numpy(A).to(f"cuda:{device}"), opts=exec_opts(mode, act_scheme.group_size), err=err)
+    torch.cuda.synchronize(device)
+    e = int(err.item())
+    if e != 2**31 - 1:
+        G = (layer.in_features + act_scheme.group_size - 1) // act_scheme.group_size
+        raise DataError(f"row {e // G}, group {e % G}: quantize: non-finite input value")
+    return Y.cpu().numpy()
+
+
+def run_bench(m: int, n: int, k: int, percent: float = 0.1, group_size: int = 128, repeats: int = 3,
+              seed: int = 1, mode: int = capi.MQ_EXACT, device: int = 0) -> dict:
+    """run_bench (gemm.cpp:206-259) on the B200: same generator, same
+    checksum definition (FNV-1a over the f32 output), CUDA-event timing of
+    the device forward (activation quantization + GEMM + scatter)."""
+    import torch
+    W, A, prom = bench_inputs(m, n, k, percent, seed)
+    layer = partition_and_quantize(W, prom, QuantScheme(8, True, group_size), QuantScheme(4, False, group_size), "bench")
+    dl = DeviceLayer(layer, device)
+    dA = torch.from_numpy(A).to(f"cuda:{device}")
+    opts = exec_opts(mode, group_size)
+    Y = dl.forward(dA, opts=opts)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(repeats):
+        dl.forward(dA, out=Y, opts=opts)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / repeats
+    out = Y.cpu().numpy()
+    return dict(m=m, n=n, k=k, percent=percent, group_size=group_size, repeats=repeats, wall_ms=ms,
+                gops=2.0 * m * n * k / (ms * 1e6), checksum=fnv1a_hex(out))
