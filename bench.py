@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py — MixLLM W4/W8-A8 mixed-precision linear on B200.
+
+Workload (BASELINE.json configs[1]): the Llama-3.1-8B decoder-layer linear
+stack (q, k, v, o, gate, up, down), 10% of output features 8-bit, 4-bit
+group-128 weights, int8 group-wise activations (the reference's semantics,
+proj/src/gemm.cpp:183-192), MQ_FAST mode, fp16 output, batch M (default 16).
+One STEP = the 7 projections' full dynamic path (activation quantization +
+mixed GEMM + scatter) = 14 kernel launches, replayed from a CUDA graph.
+Synthetic run_bench-generator weights/activations (no checkpoints). Two
+device replicas of the stack (2 x ~128 MB) alternate between steps so the
+weights stream from HBM, not L2 (126 MB).
+
+N > 1 (torchrun): the stack is column-sharded by output feature (each rank
+owns a slice of both the 4-bit and 8-bit partitions), activations replicated,
+outputs all-gathered over NCCL and permuted back: strong scaling.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+proj/ sources compiled unmodified) on the host cores, same workload, rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import numpy as np  # noqa: E402
+
+SHAPES_8B = [("q_proj", 4096, 4096), ("k_proj", 1024, 4096), ("v_proj", 1024, 4096), ("o_proj", 4096, 4096),
+             ("gate_proj", 14336, 4096), ("up_proj", 14336, 4096), ("down_proj", 4096, 14336)]
+PERCENT = 0.10
+GROUP = 128
+METRIC = "mixed-precision linear TOPS & latency vs batch (1-512); % HBM / int8-TC peak"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def k2_bytes(M, N, K, n8, n4, out_bytes=2):
+    """SURVEY §8d algorithmic bytes of one mixed-GEMM launch."""
+    G = (K + GROUP - 1) // GROUP
+    return K * (n4 / 2 + n8) + G * (4 * N + n4) + M * K + 4 * M * G + M * N * out_bytes
+
+
+def k1_bytes(M, K):
+    G = (K + GROUP - 1) // GROUP
+    return M * K * 4 + M * K + 4 * M * G
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measure_int8_peak(torch):
+    """Dense int8 tensor-core reference: torch._int_mm on 8192^3 (best of 10)."""
+    try:
+        a = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+        b = torch.randint(-127, 127, (8192, 8192), dtype=torch.int8, device="cuda")
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = 1e30
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_14590_b200 as mq
+    from paper_2412_14590_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    M = args.batch
+    hbm_peak, peak_kind = peaks()
+
+    # ---- host: quantize the stack once (reference layouts, bit-exact)
+    host = []
+    for i, (name, N, K) in enumerate(SHAPES_8B):
+        W, A, prom = mq.bench_inputs(1, N, K, PERCENT, 1 + i)
+        host.append((name, N, K, mq.partition_and_quantize(W, prom, name=name)))
+    R = 2 if world == 1 else 1  # device replicas rotated between steps (> L2)
+    layers = [[mq.DeviceLayer(L, local, rank=rank, world=world) for (_, _, _, L) in host] for _ in range(R)]
+    mode = capi.MQ_FAST if args.mode == "fast" else capi.MQ_EXACT
+
+    def make_io(m, act_group):
+        g = torch.Generator(device=dev).manual_seed(1234 + m)
+        xs = [torch.randn((m, K), generator=g, device=dev, dtype=torch.float32) for (_, _, K, _) in host]
+        ys = [torch.empty((m, layers[0][i].out_cols), dtype=torch.float16, device=dev) for i in range(len(host))]
+        opts = mq.exec_opts(mode, act_group)
+        return xs, ys, opts
+
+    colmaps, gathered, finals = None, None, None
+    if world > 1:
+        colmaps = [torch.from_numpy(layers[0][i].shard_colmap()).to(dev) for i in range(len(host))]
+
+    def step(r, xs, ys, opts, m):
+        for i in range(len(host)):
+            layers[r][i].forward(xs[i], out=ys[i], opts=opts)
+            if world > 1:
+                dist.all_gather_into_tensor(gathered[i], ys[i])
+                mq.permute_gathered(gathered[i], colmaps[i], world, layers[r][i].out_cols, m, host[i][1],
+                                    out=finals[i])
+
+    def step_codes(r, cs, ys, opts):
+        for i in range(len(host)):
+            layers[r][i].forward_codes(cs[i][0], cs[i][1], out=ys[i], opts=opts)
+
+    def timed(fn_list, steps, warmup):
+        for i in range(warmup):
+            fn_list[i % len(fn_list)]()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(steps):
+            fn_list[i % len(fn_list)]()
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item()) / steps
+
+    def graphs_for(fn_of_r):
+        out = []
+        for r in range(R):
+            fn_of_r(r)  # eager warm-up: workspaces, attributes
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn_of_r(r)
+            out.append(g.replay)
+        return out
+
+    def bench_batch(m, act_group, steps, warmup, sampler=None):
+        xs, ys, opts = make_io(m, act_group)
+        nonlocal gathered, finals
+        if world > 1:
+            gathered = [torch.empty((world, m, layers[0][i].out_cols), dtype=torch.float16, device=dev)
+                        for i in range(len(host))]
+            finals = [torch.empty((m, host[i][1]), dtype=torch.float16, device=dev) for i in range(len(host))]
+            fns = [lambda r=r: step(r, xs, ys, opts, m) for r in range(R)]  # eager (NCCL)
+            for f in fns:
+                f()
+        else:
+            fns = graphs_for(lambda r: step(r, xs, ys, opts, m))
+        def ramp():  # pre-ramp clocks (not counted as steps)
+            t_end = time.time() + 0.3
+            while time.time() < t_end:
+                fns[0]()
+                torch.cuda.synchronize()
+
+        if sampler:
+            with sampler:
+                ramp()
+                ms = timed(fns, steps, warmup)
+        else:
+            ramp()
+            ms = timed(fns, steps, warmup)
+        # K2-only timing (the dominant kernel), same graphs minus K1
+        cs = [mq.quantize_act(x, act_group if act_group < x.shape[1] else x.shape[1]) for x in xs]
+        k2fns = graphs_for(lambda r: step_codes(r, cs, ys, opts)) if world == 1 else \
+            [lambda r=r: step_codes(r, cs, ys, opts) for r in range(R)]
+        ms_k2 = timed(k2fns, steps, warmup)
+        ops = sum(2.0 * m * N * K for (_, N, K, _) in host)
+        b2 = sum(k2_bytes(m, N // world if world > 1 else N, K, L.sub8.rows // world, L.sub4.rows // world)
+                 for (_, N, K, L) in host)
+        b1 = sum(k1_bytes(m, K) for (_, _, K, _) in host)
+        return dict(ms=ms, ms_k2=ms_k2, ops=ops, k2_bytes=b2, k1_bytes=b1, xs=xs, ys=ys, opts=opts)
+
+    int8_peak = measure_int8_peak(torch) if rank == 0 else None
+    sampler = ClockSampler(local)
+    head = bench_batch(M, GROUP, args.steps, args.warmup, sampler)
+    ms = head["ms"]
+    value = head["ops"] / (ms * 1e-3) / 1e12
+    achieved = head["k2_bytes"] / (head["ms_k2"] * 1e-3) / 1e9  # GB/s over the 7 K2 launches
+
+    # ---- e2e through the public C-ABI path with host buffers (pinned), N GPUs
+    e2e = None
+    if world == 1:
+        xs, ys = head["xs"], head["ys"]
+        hx = [x.cpu().pin_memory() for x in xs]
+        hy = [torch.empty(y.shape, dtype=y.dtype).pin_memory() for y in ys]
+
+        def e2e_step(r):
+            for i in range(len(host)):
+                xs[i].copy_(hx[i], non_blocking=True)
+                layers[r][i].forward(xs[i], out=ys[i], opts=head["opts"])
+                hy[i].copy_(ys[i], non_blocking=True)
+
+        efns = graphs_for(e2e_step)
+        ems = timed(efns, args.steps, args.warmup)
+        e2e = {"value": head["ops"] / (ems * 1e-3) / 1e12, "unit": "TOPS",
+               "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in hx)),
+               "d2h_bytes_per_step": int(sum(y.numel() * 2 for y in hy)), "ms_per_step": ems}
+
+    # ---- batch sweep (BASELINE metric is "vs batch 1-512")
+    sweep = {}
+    if world == 1 and not args.no_sweep:
+        for m in (1, 16, 64, 256, 512):
+            for ag_name, ag in (("group", GROUP), ("token", 1 << 30)):
+                if ag_name == "token" and m not in (16, 512):
+                    continue
+                r = bench_batch(m, ag, max(10, args.steps // 4), 3)
+                key = f"M{m}" + ("" if ag_name == "group" else "_per_token")
+                t2 = r["ms_k2"] * 1e-3
+                sweep[key] = {"tops": round(r["ops"] / (r["ms"] * 1e-3) / 1e12, 2),
+                              "us_per_layer": round(r["ms"] * 1e3, 2),
+                              "k2_us_per_layer": round(r["ms_k2"] * 1e3, 2),
+                              "k2_hbm_frac": round(r["k2_bytes"] / t2 / 1e9 / hbm_peak, 3),
+                              "k2_int8_tc_frac": (round(r["ops"] / t2 / 1e12 / int8_peak, 3) if int8_peak else None)}
+                del r
+
+    # ---- CPU baseline (rank 0, N = 1 only): the reference on the host cores
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_reference(M, budget_s=args.cpu_budget)
+
+    clocks = sampler.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int8 (int32 accum, f32 rescale, f16 out)",
+            "data": "synthetic (run_bench generator weights, randn activations)",
+            "config": {"workload": f"llama3.1-8b decoder-layer linear stack q,k,v,o,gate,up,down; batch {M}; "
+                                   f"{int(PERCENT * 100)}% 8-bit output features; W4 g128 asym + W8 sym; "
+                                   f"A8 group-wise (reference semantics); mode {args.mode}; fp16 out",
+                       "batch": M, "group": GROUP, "percent_8bit": PERCENT,
+                       "parallelism": f"column-shard x{world}" if world > 1 else "single",
+                       "l2": "2 device replicas of the stack (~256 MB) alternate between steps (> 126 MB L2)",
+                       "cuda_graph": world == 1},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                         "kernel": "mixed_gemm_tc_kernel (7 launches/step; bytes and time summed)",
+                         "peak_kind": peak_kind,
+                         "k2_bytes_per_step": int(head["k2_bytes"]), "k2_ms_per_step": round(head["ms_k2"], 5)},
+            "int8_peak_tops_measured": round(int8_peak, 1) if int8_peak else None,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps * 14, "clocks": clocks,
+            "sweep": sweep,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------- reference
+def cpu_reference(M, budget_s=12.0, steps=None, warmup=0):
+    """The reference's own implementation (oracle/_ref) on this host's cores:
+    one step = execute_mixed_linear for the 7 projections (workers = nproc)."""
+    import oracle_py as O
+
+    cores = os.cpu_count() or 1
+    if O.ref_available():
+        kind = "reference"
+    else:
+        return {"value": None, "unit": "TOPS", "cores": cores, "kind": "unavailable",
+                "sample": "oracle/_ref not built (needs /root/reference at build time)"}
+    layers = []
+    for i, (name, N, K) in enumerate(SHAPES_8B):
+        W, A, prom = O.bench_inputs(M, N, K, PERCENT, 1 + i)
+        layers.append((O.RefLayer(W, prom, GROUP), A, N, K))
+    ops = sum(2.0 * M * N * K for (_, _, N, K) in layers)
+
+    def one():
+        t = 0.0
+        for (R, A, _, _) in layers:
+            _, ms = R.forward(A, fast=True, workers=cores)
+            t += ms
+        return t
+
+    for _ in range(warmup):
+        one()
+    times = []
+    t0 = time.time()
+    while True:
+        times.append(one())
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and time.time() - t0 > budget_s:
+            break
+    ms = sum(times) / len(times)
+    return {"value": round(ops / (ms * 1e-3) / 1e12, 6), "unit": "TOPS", "cores": cores, "kind": kind,
+            "ms_per_step": round(ms, 2),
+            "sample": f"{len(times)} step(s) of the full 7-projection stack at batch {M} "
+                      f"(reference execute_mixed_linear, workers={cores}, fast I2F)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # bound the run: each step is the whole stack (~1 s at M=16 on 8 cores)
+    budget_steps = max(1, min(args.steps, 20))
+    res = cpu_reference(args.batch, steps=budget_steps, warmup=min(args.warmup, 1))
+    line = {"metric": METRIC, "impl": "reference", "value": res["value"], "unit": "TOPS",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": budget_steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": res.get("ms_per_step"), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int8 (int32 accum, f32 rescale, f32 out)", "data": "synthetic",
+            "config": {"workload": f"llama3.1-8b decoder-layer linear stack q,k,v,o,gate,up,down; batch {args.batch}; "
+                                   f"{int(PERCENT * 100)}% 8-bit output features; W4 g128 asym + W8 sym; "
+                                   f"A8 group-wise (reference semantics); reference CPU path",
+                       "batch": args.batch},
+            "cpu_baseline": {"value": res["value"], "unit": "TOPS", "cores": res["cores"], "kind": res["kind"],
+                             "sample": res["sample"]},
+            "e2e": {"value": res["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if budget_steps != args.steps:
+        line["note"] = f"steps capped at {budget_steps} (each step is the whole CPU stack)"
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

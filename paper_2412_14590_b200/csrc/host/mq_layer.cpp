@@ -74,15 +74,18 @@ int auto_token_tile(int64_t M) {
     return 128;
 }
 
-// Split-K choice for MQ_FAST: balance CTA waves against per-unit group count.
-int auto_ksplit(int64_t units1, int G, int sms) {
+// Split-K choice for MQ_FAST. Cost in units of "one weight group streamed":
+// waves x (groups per unit + fixed unit cost + partial-tile round trip), the
+// partial tile (128 x bn f32) weighing bn*512 B against ~8.8 KB per group.
+int auto_ksplit(int64_t units1, int G, int sms, int bn) {
     int best = 1;
     double best_cost = 1e30;
+    const double part = bn * 512.0 / 8832.0;
     for (int s = 1; s <= std::min(G, 16); ++s) {
         const int64_t units = units1 * s;
         const int64_t waves = (units + sms - 1) / sms;
         const int64_t per = (G + s - 1) / s;
-        const double cost = double(waves * per) + 0.35 * (s > 1 ? 1.0 : 0.0) + 0.02 * s;
+        const double cost = double(waves) * (double(per) + 2.0 + (s > 1 ? part : 0.0)) + 0.02 * s;
         if (cost < best_cost - 1e-9) {
             best_cost = cost;
             best = s;
@@ -116,7 +119,7 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
         pl->ksplit = 1;
         pl->mode = kExactGroup;
     } else {
-        pl->ksplit = o->ksplit ? std::min(o->ksplit, L->G) : auto_ksplit(tiles * pl->tb, L->G, L->num_sms);
+        pl->ksplit = o->ksplit ? std::min(o->ksplit, L->G) : auto_ksplit(tiles * pl->tb, L->G, L->num_sms, pl->bn);
         pl->mode = pl->sa_cols == 1 ? kFastToken : kFastGroup;
     }
     if (pl->ksplit < 1) pl->ksplit = 1;

@@ -377,8 +377,14 @@ cudaError_t launch_bn_mode(const GemmParams& p, const void* tmap, int num_sms, c
     NS = NS > kMaxStages ? kMaxStages : NS;
     const size_t smem = C::kFixedSmem + size_t(NS) * C::kStageBytes;
     auto kern = mixed_gemm_tc_kernel<BN, MODE>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
+    static thread_local uint64_t configured = 0;  // per device ordinal bitmask
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(configured >> dev & 1)) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        configured |= uint64_t(1) << dev;
+    }
     const int units = p.num_tiles * p.token_blocks * p.ksplit;
     const int grid = units < num_sms ? units : num_sms;
     if (grid <= 0) return cudaSuccess;
