@@ -168,13 +168,17 @@ mq_status mq_layer_shard_colmap(mq_layer_t layer, int32_t* out);
  * A: device [M, K] (row stride lda elements) in a_dtype. group_size == the
  * layer group (reference, group-wise) or == K (per-token, north_star). codes:
  * device int8 [M, ldc] (ldc >= K, multiple of 16; columns K..ldc are zeroed);
- * scales: device f32 [M, G] (group-wise, reference layout) or [M] (per-token).
+ * scales: device f32, group-major [G, lds] (group-wise) or [M] (per-token).
  * err (nullable, device int32, caller initialises to INT32_MAX): receives the
  * smallest m*G+g whose group held a non-finite value (the reference's
- * DataError, quant.hpp:56-64). Bit-exact with the reference for f32 input. */
+ * DataError, quant.hpp:56-64). Bit-exact with the reference for f32 input.
+ * Scales are written GROUP-MAJOR, scales[g * lds + m] (lds >= M), so each
+ * K-group's token scales are one contiguous run the GEMM producer streams
+ * with a bulk copy (the reference keeps [M, G]; the values are identical).
+ * Per-token: scales[m]. */
 mq_status mq_quantize_act(const void* A, mq_dtype a_dtype, int64_t M, int64_t K, int64_t lda,
                           int32_t group_size, int8_t* codes, int64_t ldc, float* scales,
-                          int32_t* err, void* stream);
+                          int64_t lds, int32_t* err, void* stream);
 
 /* Forward modes.
  * MQ_EXACT: per output element the K-groups run in ascending order with an f32
@@ -187,9 +191,10 @@ typedef enum { MQ_EXACT = 0, MQ_FAST = 1 } mq_mode;
 typedef struct {
     int32_t mode;        /* mq_mode */
     int32_t act_group;   /* group size the activation scales use (g or K) */
-    int32_t ksplit;      /* 0 = auto (MQ_FAST only) */
+    int32_t ksplit;      /* 0 = auto stream-K (MQ_FAST); 1 = no K splitting */
     int32_t token_tile;  /* 0 = auto; else 16/32/64/128 */
     int32_t gemm_impl;   /* 0 = tcgen05 (product); 1 = SIMT debug kernel */
+    int32_t no_pdl;      /* 1 = plain launches (default: programmatic dependent launch) */
 } mq_exec_opts;
 
 /* Bytes of scratch a forward needs (split-K partials + counters). */
@@ -198,15 +203,17 @@ size_t mq_forward_workspace_bytes(mq_layer_t layer, int64_t M, const mq_exec_opt
 /* The mixed-precision linear on quantized activations
  * (execute_mixed_on_codes, gemm.cpp:140-181): both sub-problems in one
  * persistent launch, scatter fused into the epilogue.
- * codes: device int8 [M, ldc]; scales as mq_quantize_act wrote them;
+ * codes: device int8 [M, ldc] (16-byte aligned, ldc % 16 == 0); scales as
+ * mq_quantize_act wrote them (group-major, lds % 4 == 0, 16-byte aligned);
  * Y: device [M, out_features] row-major in out_dtype (sharded layers: the
  * rank's [M, shard_cols] block in gather order).
  * workspace: device, >= mq_forward_workspace_bytes, zero-initialised once
  * before first use (the engine leaves it zeroed). NULL uses the layer's own
  * (then calls on one layer must be stream-serialised). */
 mq_status mq_mixed_linear_codes(mq_layer_t layer, const int8_t* codes, int64_t ldc,
-                                const float* scales, int64_t M, void* Y, mq_dtype out_dtype,
-                                const mq_exec_opts* opts, void* workspace, void* stream);
+                                const float* scales, int64_t lds, int64_t M, void* Y,
+                                mq_dtype out_dtype, const mq_exec_opts* opts, void* workspace,
+                                void* stream);
 
 /* The full dynamic path (execute_mixed_linear, gemm.cpp:183-192): activation
  * quantization + mixed GEMM + scatter. A: device [M, K] f32/f16/bf16.

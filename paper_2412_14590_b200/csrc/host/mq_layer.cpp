@@ -1,5 +1,6 @@
 // mq_layer.cpp — device layer handle, the one-time packer into the engine's
-// HBM layout (mq_layout.cuh) and the forward entry points of the C ABI.
+// HBM layout (mq_layout.cuh), the stream-K scheduler and the forward entry
+// points of the C ABI.
 //
 // The reference re-prepacks both sub-problems on every forward call
 // (proj/src/gemm.cpp:148-149, ~45% of its call time at M=16); here
@@ -10,7 +11,9 @@
 
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -19,6 +22,16 @@
 #include "mq_internal.hpp"
 
 using namespace mq;
+
+namespace {
+struct Sched {
+    int grid = 0;
+    int slots = 0;        // stream-K partial tiles
+    int64_t items = 0;    // (tile, token block) work items
+    Seg* d_segs = nullptr;
+    int32_t* d_cta = nullptr;
+};
+}  // namespace
 
 struct mq_layer_s {
     int device = 0;
@@ -38,9 +51,9 @@ struct mq_layer_s {
     int64_t bytes_wq = 0, bytes_meta = 0, stream_bytes = 0;
     std::vector<TileDesc> tiles;
     std::vector<int32_t> shard_colmap;  // [world * shard_cols]
-    // internal scratch (used when the caller passes workspace = NULL)
-    std::mutex ws_mu;
-    void* d_ws = nullptr;
+    std::mutex mu;                      // guards the caches below
+    std::map<int64_t, Sched> scheds;    // keyed by (bn, token blocks, split)
+    void* d_ws = nullptr;               // internal scratch (workspace = NULL)
     size_t ws_bytes = 0;
 };
 
@@ -49,10 +62,10 @@ namespace {
 mq_status cuda_fail(cudaError_t e, const char* what) {
     return fail(MQ_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
-#define CU_TRY(expr)                                                  \
-    do {                                                              \
-        cudaError_t _e = (expr);                                      \
-        if (_e != cudaSuccess) return cuda_fail(_e, #expr);           \
+#define CU_TRY(expr)                                        \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
     } while (0)
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -74,62 +87,129 @@ int auto_token_tile(int64_t M) {
     return 128;
 }
 
-// Split-K choice for MQ_FAST. Cost in units of "one weight group streamed":
-// waves x (groups per unit + fixed unit cost + partial-tile round trip), the
-// partial tile (128 x bn f32) weighing bn*512 B against ~8.8 KB per group.
-int auto_ksplit(int64_t units1, int G, int sms, int bn) {
-    int best = 1;
-    double best_cost = 1e30;
-    const double part = bn * 512.0 / 8832.0;
-    for (int s = 1; s <= std::min(G, 16); ++s) {
-        const int64_t units = units1 * s;
-        const int64_t waves = (units + sms - 1) / sms;
-        const int64_t per = (G + s - 1) / s;
-        const double cost = double(waves) * (double(per) + 2.0 + (s > 1 ? part : 0.0)) + 0.02 * s;
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = s;
+// ---------------------------------------------------------------- schedule
+// Weighted stream-K over work items (tile, token block) x K-groups: every CTA
+// gets ~1/P of the total streamed bytes (sub8 groups cost ~2x sub4 groups).
+// split=false (MQ_EXACT, dumps) keeps every item whole on one CTA so the
+// reference's ascending-group f32 accumulation order is preserved.
+void build_schedule(const std::vector<TileDesc>& tiles, int G, int bn, int tb, bool split, int sms,
+                    std::vector<Seg>& segs, std::vector<int32_t>& cta, int* slots) {
+    const int64_t T = static_cast<int64_t>(tiles.size());
+    auto gcost = [&](int64_t t) {
+        const TileDesc& td = tiles[t];
+        return double(td.copy_bytes + (td.is8 ? kMeta8Bytes : kMeta4Bytes)) + bn * 128.0 + 1024.0;
+    };
+    double total = 0;
+    for (int64_t t = 0; t < T; ++t) total += gcost(t) * G * tb;
+    const int64_t items = T * tb;
+    int P = sms;
+    if (!split) P = static_cast<int>(std::min<int64_t>(P, items));
+    else P = static_cast<int>(std::min<int64_t>(P, items * G));
+    P = std::max(P, 1);
+    const double target = total / P;
+    segs.clear();
+    cta.assign(1, 0);
+    double acc = 0;
+    int c = 0;
+    for (int64_t t = 0; t < T; ++t) {
+        const double gc = gcost(t);
+        for (int b = 0; b < tb; ++b) {
+            if (!split) {
+                segs.push_back(Seg{int32_t(t), b, 0, G, 1, 0, -1, 0});
+                acc += gc * G;
+                if (acc >= (c + 1) * target - 0.5 * gc && c < P - 1) {
+                    ++c;
+                    cta.push_back(static_cast<int32_t>(segs.size()));
+                }
+                continue;
+            }
+            int g = 0;
+            while (g < G) {
+                const double cap = (c + 1) * target - acc;
+                int k = static_cast<int>(std::floor(cap / gc + 0.5));
+                k = std::max(k, 1);
+                k = std::min(k, G - g);
+                if (G - g - k > 0 && G - g - k < 2) k = G - g;  // no 1-group tails
+                segs.push_back(Seg{int32_t(t), b, g, g + k, 1, 0, -1, 0});
+                acc += gc * k;
+                g += k;
+                if (acc >= (c + 1) * target - 0.5 * gc && c < P - 1) {
+                    ++c;
+                    cta.push_back(static_cast<int32_t>(segs.size()));
+                }
+            }
         }
     }
-    return best;
+    if (cta.back() != static_cast<int32_t>(segs.size())) cta.push_back(static_cast<int32_t>(segs.size()));
+    // segments of one item are contiguous: number them, give split ones slots
+    int s = 0;
+    for (size_t i = 0; i < segs.size();) {
+        size_t j = i;
+        while (j < segs.size() && segs[j].tile == segs[i].tile && segs[j].tb == segs[i].tb) ++j;
+        const int n = static_cast<int>(j - i);
+        for (size_t q = i; q < j; ++q) {
+            segs[q].nseg = n;
+            segs[q].sidx = static_cast<int32_t>(q - i);
+            segs[q].pslot = n > 1 ? s++ : -1;
+        }
+        i = j;
+    }
+    *slots = s;
+}
+
+mq_status get_sched(mq_layer_s* L, int bn, int tb, bool split, cudaStream_t stream, const Sched** out) {
+    const int64_t key = (int64_t(tb) << 16) | (int64_t(bn) << 1) | (split ? 1 : 0);
+    std::lock_guard<std::mutex> lk(L->mu);
+    auto it = L->scheds.find(key);
+    if (it != L->scheds.end()) {
+        *out = &it->second;
+        return MQ_OK;
+    }
+    cudaStreamCaptureStatus cs;
+    if (stream && cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+        return fail(MQ_USAGE, "first forward of a (batch, mode) plan cannot be graph-captured; run it once eagerly");
+    std::vector<Seg> segs;
+    std::vector<int32_t> cta;
+    Sched sc;
+    build_schedule(L->tiles, L->G, bn, tb, split, L->num_sms, segs, cta, &sc.slots);
+    sc.grid = static_cast<int>(cta.size()) - 1;
+    sc.items = static_cast<int64_t>(L->tiles.size()) * tb;
+    CU_TRY(cudaMalloc(&sc.d_segs, std::max<size_t>(segs.size(), 1) * sizeof(Seg)));
+    CU_TRY(cudaMalloc(&sc.d_cta, cta.size() * sizeof(int32_t)));
+    CU_TRY(cudaMemcpy(sc.d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemcpy(sc.d_cta, cta.data(), cta.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    *out = &(L->scheds[key] = sc);
+    return MQ_OK;
 }
 
 struct Plan {
-    int bn, tb, ksplit, mode, sa_cols;
-    size_t ws_floats, counters;
+    int bn, tb, mode, per_token;
+    bool split, pdl;
 };
 
 mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
     mq_exec_opts d{};
-    d.act_group = L->group;
     if (!o) o = &d;
     const int act_group = o->act_group ? o->act_group : L->group;
-    if (act_group == L->group) pl->sa_cols = L->G;
-    else if (act_group >= L->K) pl->sa_cols = 1;
-    else return fail(MQ_USAGE, "activations and weights must share group boundaries (act group " +
-                                   std::to_string(act_group) + ", weight group " + std::to_string(L->group) +
-                                   "); per-token activations use act_group = K");
+    if (act_group == L->group && act_group < L->K) pl->per_token = 0;
+    else if (act_group >= L->K) pl->per_token = 1;
+    else
+        return fail(MQ_USAGE, "activations and weights must share group boundaries (act group " +
+                                  std::to_string(act_group) + ", weight group " + std::to_string(L->group) +
+                                  "); per-token activations use act_group = K");
     if (o->mode != MQ_EXACT && o->mode != MQ_FAST) return fail(MQ_USAGE, "unknown mode");
     pl->bn = o->token_tile ? o->token_tile : auto_token_tile(M);
     if (pl->bn != 16 && pl->bn != 32 && pl->bn != 64 && pl->bn != 128)
         return fail(MQ_USAGE, "token_tile must be 16, 32, 64 or 128");
     pl->tb = static_cast<int>((M + pl->bn - 1) / pl->bn);
-    const int64_t tiles = L->tiles8 + L->tiles4;
-    if (o->mode == MQ_EXACT) {
-        pl->ksplit = 1;
-        pl->mode = kExactGroup;
-    } else {
-        pl->ksplit = o->ksplit ? std::min(o->ksplit, L->G) : auto_ksplit(tiles * pl->tb, L->G, L->num_sms, pl->bn);
-        pl->mode = pl->sa_cols == 1 ? kFastToken : kFastGroup;
-    }
-    if (pl->ksplit < 1) pl->ksplit = 1;
-    pl->ws_floats = pl->ksplit > 1 ? size_t(tiles) * pl->tb * pl->ksplit * 128 * pl->bn : 0;
-    pl->counters = pl->ksplit > 1 ? size_t(tiles) * pl->tb : 0;
+    pl->split = o->mode == MQ_FAST && o->ksplit != 1;
+    pl->mode = o->mode == MQ_EXACT ? kExactGroup : (pl->per_token ? kFastToken : kFastGroup);
+    pl->pdl = o->no_pdl == 0;
     return MQ_OK;
 }
 
-size_t plan_ws_bytes(const Plan& pl) {
-    return ((pl.counters * 4 + 255) / 256) * 256 + pl.ws_floats * 4;
+size_t ws_bytes_for(const Sched& sc, int bn) {
+    return ((size_t(sc.items) * 4 + 255) / 256) * 256 + size_t(sc.slots) * 128 * bn * 4;
 }
 
 mq_status encode_act_map(CUtensorMap* map, const int8_t* codes, int64_t ldc, int64_t M, int64_t K, int bn) {
@@ -140,19 +220,14 @@ mq_status encode_act_map(CUtensorMap* map, const int8_t* codes, int64_t ldc, int
     const cuuint32_t box[2] = {128u, static_cast<cuuint32_t>(bn)};
     const cuuint32_t estr[2] = {1u, 1u};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(codes), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(MQ_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     return MQ_OK;
 }
 
-mq_status check_layer(const mq_layer_s* L) {
-    if (!L) return fail(MQ_USAGE, "layer handle is null");
-    return MQ_OK;
-}
-
-mq_status gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t M, void* Y,
-                      mq_dtype out_dtype, void* ws, GemmParams* p) {
+void gemm_params(const mq_layer_s* L, const Plan& pl, const Sched* sc, const float* sa, int64_t lds, int64_t M,
+                 void* Y, mq_dtype out_dtype, void* ws, GemmParams* p) {
     std::memset(p, 0, sizeof(*p));
     p->tiles = L->d_tiles;
     p->num_tiles = static_cast<int32_t>(L->tiles8 + L->tiles4);
@@ -162,27 +237,28 @@ mq_status gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int6
     p->wmeta = L->d_meta;
     p->colmap = L->d_colmap;
     p->sa = sa;
-    p->sa_cols = pl.sa_cols;
+    p->sa_gstride = pl.per_token ? 0 : lds;
     p->M = M;
     p->Y = Y;
     p->out_dtype = out_dtype;
     p->ldy = L->world > 1 ? L->shard_cols : L->N;
-    p->ksplit = pl.ksplit;
     p->token_blocks = pl.tb;
-    uint8_t* w = static_cast<uint8_t*>(ws);
-    p->counters = reinterpret_cast<uint32_t*>(w);
-    p->ws = reinterpret_cast<float*>(w + ((pl.counters * 4 + 255) / 256) * 256);
+    if (sc) {
+        p->segs = sc->d_segs;
+        p->cta_seg = sc->d_cta;
+        uint8_t* w = static_cast<uint8_t*>(ws);
+        p->counters = reinterpret_cast<uint32_t*>(w);
+        p->ws = reinterpret_cast<float*>(w + ((size_t(sc->items) * 4 + 255) / 256) * 256);
+    }
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
-    return MQ_OK;
 }
 
-mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, void** ws) {
-    if (bytes == 0) {
-        *ws = nullptr;
-        return MQ_OK;
-    }
-    std::lock_guard<std::mutex> lk(L->ws_mu);
+mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, cudaStream_t stream, void** ws) {
+    std::lock_guard<std::mutex> lk(L->mu);
     if (L->ws_bytes < bytes) {
+        cudaStreamCaptureStatus cs;
+        if (stream && cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+            return fail(MQ_USAGE, "internal workspace cannot grow during graph capture; pass a workspace");
         if (L->d_ws) cudaFree(L->d_ws);
         L->d_ws = nullptr;
         L->ws_bytes = 0;
@@ -192,6 +268,24 @@ mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, void** ws) {
     }
     *ws = L->d_ws;
     return MQ_OK;
+}
+
+int64_t lds_for(int64_t M) { return (M + 3) / 4 * 4; }
+
+// workspace of the full dynamic path: codes [M, ldc] | scales [Ga, lds] | gemm
+struct FullWs {
+    int64_t ldc, lds;
+    size_t off_scales, off_gemm, total;
+};
+FullWs full_ws_layout(const mq_layer_s* L, int64_t M, int per_token, size_t gemm_bytes) {
+    FullWs f;
+    f.ldc = (L->K + 127) / 128 * 128;
+    f.lds = lds_for(M);
+    const int64_t Ga = per_token ? 1 : L->G;
+    f.off_scales = size_t((M * f.ldc + 255) / 256 * 256);
+    f.off_gemm = f.off_scales + size_t((Ga * f.lds * 4 + 255) / 256 * 256);
+    f.total = f.off_gemm + gemm_bytes;
+    return f;
 }
 
 }  // namespace
@@ -339,12 +433,16 @@ void mq_layer_destroy(mq_layer_t L) {
     cudaFree(L->d_meta);
     cudaFree(L->d_tiles);
     cudaFree(L->d_colmap);
+    for (auto& kv : L->scheds) {
+        cudaFree(kv.second.d_segs);
+        cudaFree(kv.second.d_cta);
+    }
     if (L->d_ws) cudaFree(L->d_ws);
     delete L;
 }
 
 mq_status mq_layer_get_info(mq_layer_t L, mq_layer_info* info) {
-    if (mq_status st = check_layer(L)) return st;
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
     info->out_features = L->N;
     info->in_features = L->K;
     info->group_size = L->group;
@@ -361,112 +459,138 @@ mq_status mq_layer_get_info(mq_layer_t L, mq_layer_info* info) {
 }
 
 mq_status mq_layer_shard_colmap(mq_layer_t L, int32_t* out) {
-    if (mq_status st = check_layer(L)) return st;
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (L->world == 1) return fail(MQ_USAGE, "layer is not sharded");
     std::copy(L->shard_colmap.begin(), L->shard_colmap.end(), out);
     return MQ_OK;
 }
 
-mq_status mq_quantize_act(const void* A, mq_dtype dt, int64_t M, int64_t K, int64_t lda, int32_t group,
-                          int8_t* codes, int64_t ldc, float* scales, int32_t* err, void* stream) {
+mq_status mq_quantize_act(const void* A, mq_dtype dt, int64_t M, int64_t K, int64_t lda, int32_t group, int8_t* codes,
+                          int64_t ldc, float* scales, int64_t lds, int32_t* err, void* stream) {
     if (M < 0 || K < 1) return fail(MQ_USAGE, "bad activation shape");
     if (group < 1) return fail(MQ_USAGE, "group_size must be >= 1");
     if (lda < K || ldc < K) return fail(MQ_USAGE, "leading dimension smaller than K");
+    if (group < K && lds < M) return fail(MQ_USAGE, "scales leading dimension smaller than M");
     if (dt != MQ_F32 && dt != MQ_F16 && dt != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
-    cudaError_t e = launch_act_quant(A, dt, M, K, lda, group >= K ? int(K) : group, 0, codes, ldc, scales, err,
-                                     static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_act_quant(A, dt, M, K, lda, group >= K ? int(K) : group, 0, codes, ldc, scales, lds, err,
+                                     true, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
     return MQ_OK;
 }
 
 size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
     Plan pl;
-    if (!L || make_plan(L, M, o, &pl) != MQ_OK) return 0;
-    return plan_ws_bytes(pl);
+    if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK) return 0;
+    const Sched* sc = nullptr;
+    if (get_sched(L, pl.bn, pl.tb, pl.split, nullptr, &sc) != MQ_OK) return 0;
+    return ws_bytes_for(*sc, pl.bn);
 }
 
-mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, const float* scales, int64_t M,
-                                void* Y, mq_dtype out_dtype, const mq_exec_opts* o, void* ws, void* stream) {
-    if (mq_status st = check_layer(L)) return st;
+mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, const float* scales, int64_t lds,
+                                int64_t M, void* Y, mq_dtype out_dtype, const mq_exec_opts* o, void* ws,
+                                void* stream) {
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
     if (M == 0) return MQ_OK;
     if (ldc < L->K || ldc % 16 != 0) return fail(MQ_USAGE, "ldc must be >= K and a multiple of 16 (TMA row pitch)");
     if (reinterpret_cast<uintptr_t>(codes) % 16 != 0) return fail(MQ_USAGE, "codes must be 16-byte aligned");
+    if (reinterpret_cast<uintptr_t>(scales) % 16 != 0) return fail(MQ_USAGE, "scales must be 16-byte aligned");
     if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
     Plan pl;
     if (mq_status st = make_plan(L, M, o, &pl)) return st;
-    if (!ws) {
-        if (mq_status st = ensure_internal_ws(L, plan_ws_bytes(pl), &ws)) return st;
+    if (!pl.per_token && (lds < M || lds % 4 != 0))
+        return fail(MQ_USAGE, "group-wise scales need lds >= M and lds % 4 == 0 (group-major layout)");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (o && o->gemm_impl == 1) {
+        GemmParams p;
+        gemm_params(L, pl, nullptr, scales, lds, M, Y, out_dtype, nullptr, &p);
+        cudaError_t e = launch_mixed_gemm_simt(p, codes, ldc, pl.per_token && pl.mode == kFastToken ? kFastToken : kExactGroup,
+                                               L->w8_mode == MQ_W8_REFERENCE, s);
+        if (e != cudaSuccess) return cuda_fail(e, "simt launch");
+        return MQ_OK;
+    }
+    const Sched* sc = nullptr;
+    if (mq_status st = get_sched(L, pl.bn, pl.tb, pl.split, s, &sc)) return st;
+    if (!ws && sc->slots > 0) {
+        if (mq_status st = ensure_internal_ws(L, ws_bytes_for(*sc, pl.bn), s, &ws)) return st;
     }
     GemmParams p;
-    gemm_params(L, pl, scales, M, Y, out_dtype, ws, &p);
-    const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaError_t e;
-    if (o && o->gemm_impl == 1) {
-        e = launch_mixed_gemm_simt(p, codes, ldc, pl.mode == kFastToken ? kFastToken : kExactGroup,
-                                   L->w8_mode == MQ_W8_REFERENCE, s);
-    } else {
-        alignas(64) CUtensorMap map;
-        if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
-        e = launch_mixed_gemm_tc(p, &map, pl.bn, pl.mode, L->num_sms, s);
-    }
+    gemm_params(L, pl, sc, scales, lds, M, Y, out_dtype, ws, &p);
+    alignas(64) CUtensorMap map;
+    if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
+    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, pl.mode, sc->grid, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
     return MQ_OK;
 }
 
 size_t mq_mixed_linear_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
-    if (!L) return 0;
-    const int64_t ldc = (L->K + 127) / 128 * 128;
-    const int act_group = (o && o->act_group) ? o->act_group : L->group;
-    const int64_t sa_cols = act_group >= L->K ? 1 : L->G;
-    const size_t head = size_t((M * ldc + 255) / 256 * 256) + size_t((M * sa_cols * 4 + 255) / 256 * 256);
-    return head + mq_forward_workspace_bytes(L, M, o);
+    Plan pl;
+    if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK) return 0;
+    return full_ws_layout(L, M, pl.per_token, mq_forward_workspace_bytes(L, M, o)).total;
 }
 
 mq_status mq_mixed_linear(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t M, void* Y, mq_dtype out_dtype,
                           const mq_exec_opts* o, void* ws, int32_t* err, void* stream) {
-    if (mq_status st = check_layer(L)) return st;
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (M == 0) return MQ_OK;
-    mq_exec_opts d{};
-    if (!o) o = &d;
-    const int act_group = o->act_group ? o->act_group : L->group;
     Plan pl;
     if (mq_status st = make_plan(L, M, o, &pl)) return st;
-    const int64_t ldc = (L->K + 127) / 128 * 128;
-    const size_t need = mq_mixed_linear_workspace_bytes(L, M, o);
+    const FullWs f = full_ws_layout(L, M, pl.per_token, mq_forward_workspace_bytes(L, M, o));
     if (!ws) {
-        if (mq_status st = ensure_internal_ws(L, need, &ws)) return st;
+        if (mq_status st = ensure_internal_ws(L, f.total, static_cast<cudaStream_t>(stream), &ws)) return st;
     }
     uint8_t* w = static_cast<uint8_t*>(ws);
     int8_t* codes = reinterpret_cast<int8_t*>(w);
-    const int64_t sa_cols = pl.sa_cols;
-    float* scales = reinterpret_cast<float*>(w + (M * ldc + 255) / 256 * 256);
-    void* gws = w + (M * ldc + 255) / 256 * 256 + (M * sa_cols * 4 + 255) / 256 * 256;
-    if (mq_status st = mq_quantize_act(A, a_dtype, M, L->K, L->K, act_group >= L->K ? int32_t(L->K) : act_group,
-                                       codes, ldc, scales, err, stream))
-        return st;
-    return mq_mixed_linear_codes(L, codes, ldc, scales, M, Y, out_dtype, o, gws, stream);
+    float* scales = reinterpret_cast<float*>(w + f.off_scales);
+    const int32_t ag = pl.per_token ? int32_t(L->K) : int32_t(L->group);
+    if (a_dtype != MQ_F32 && a_dtype != MQ_F16 && a_dtype != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
+    cudaError_t e = launch_act_quant(A, a_dtype, M, L->K, L->K, ag, 0, codes, f.ldc, scales, f.lds, err, pl.pdl,
+                                     static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
+    return mq_mixed_linear_codes(L, codes, f.ldc, scales, f.lds, M, Y, out_dtype, o, w + f.off_gemm, stream);
 }
 
-mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64_t M, int32_t which,
-                           int32_t* partials, void* stream) {
-    if (mq_status st = check_layer(L)) return st;
+mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64_t M, int32_t which, int32_t* partials,
+                           void* stream) {
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (which != 0 && which != 1) return fail(MQ_USAGE, "which must be 0 (sub8) or 1 (sub4)");
     if (ldc < L->K || ldc % 16 != 0) return fail(MQ_USAGE, "ldc must be >= K and a multiple of 16");
     if (M == 0) return MQ_OK;
     Plan pl;
     if (mq_status st = make_plan(L, M, nullptr, &pl)) return st;
+    const int64_t t0 = which == 0 ? 0 : L->tiles8;
+    const int64_t nt = which == 0 ? L->tiles8 : L->tiles4;
+    if (nt == 0) return MQ_OK;
+    // debug path: one whole item per CTA, schedule built per call
+    std::vector<TileDesc> sub(L->tiles.begin() + t0, L->tiles.begin() + t0 + nt);
+    std::vector<Seg> segs;
+    std::vector<int32_t> cta;
+    int slots = 0;
+    build_schedule(sub, L->G, pl.bn, pl.tb, false, 1 << 20, segs, cta, &slots);
+    Seg* d_segs = nullptr;
+    int32_t* d_cta = nullptr;
+    CU_TRY(cudaMalloc(&d_segs, segs.size() * sizeof(Seg)));
+    CU_TRY(cudaMalloc(&d_cta, cta.size() * sizeof(int32_t)));
+    CU_TRY(cudaMemcpy(d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice));
+    CU_TRY(cudaMemcpy(d_cta, cta.data(), cta.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     GemmParams p;
-    gemm_params(L, pl, nullptr, M, nullptr, MQ_F32, nullptr, &p);
-    p.tiles = L->d_tiles + (which == 0 ? 0 : L->tiles8);
-    p.num_tiles = static_cast<int32_t>(which == 0 ? L->tiles8 : L->tiles4);
-    if (p.num_tiles == 0) return MQ_OK;
-    p.ksplit = 1;
+    gemm_params(L, pl, nullptr, nullptr, 0, M, nullptr, MQ_F32, nullptr, &p);
+    p.tiles = L->d_tiles + t0;
+    p.num_tiles = static_cast<int32_t>(nt);
+    p.segs = d_segs;
+    p.cta_seg = d_cta;
     p.partials = partials;
     p.partial_rows = static_cast<int32_t>(which == 0 ? L->n8 : L->n4);
     alignas(64) CUtensorMap map;
-    if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
-    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, kDumpPartials, L->num_sms, static_cast<cudaStream_t>(stream));
+    mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn);
+    cudaError_t e = cudaSuccess;
+    if (st == MQ_OK)
+        e = launch_mixed_gemm_tc(p, &map, pl.bn, kDumpPartials, static_cast<int>(cta.size()) - 1, false,
+                                 static_cast<cudaStream_t>(stream));
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    cudaFree(d_segs);
+    cudaFree(d_cta);
+    if (st != MQ_OK) return st;
     if (e != cudaSuccess) return cuda_fail(e, "partials launch");
     return MQ_OK;
 }

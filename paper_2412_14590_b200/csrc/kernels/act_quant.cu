@@ -20,6 +20,9 @@
 namespace mq {
 namespace {
 
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <int DT>
 __device__ __forceinline__ float load_act(const void* A, int64_t i) {
     if constexpr (DT == 0) return __ldg(static_cast<const float*>(A) + i);
@@ -48,7 +51,9 @@ template <int DT>
 __global__ void act_quant_group_kernel(const void* __restrict__ A, int64_t M, int64_t K,
                                        int64_t lda, int group, int G, int f16,
                                        int8_t* __restrict__ codes, int64_t ldc,
-                                       float* __restrict__ scales, int32_t* err) {
+                                       float* __restrict__ scales, int64_t lds, int32_t* err) {
+    griddep_wait();
+    griddep_launch();
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= M * G) return;
@@ -71,7 +76,7 @@ __global__ void act_quant_group_kernel(const void* __restrict__ A, int64_t M, in
     const float s = act_scale(amax, f16);
     int8_t* crow = codes + m * ldc + b;
     for (int i = lane; i < len; i += 32) crow[i] = quant_one(load_act<DT>(A, base + i), s);
-    if (lane == 0) scales[m * G + g] = s;
+    if (lane == 0) scales[int64_t(g) * lds + m] = s;  // group-major (TMA-able per group)
     // zero the padding columns [K, ldc) once per row (owned by the last group)
     if (g == G - 1)
         for (int64_t c = K + lane; c < ldc; c += 32) codes[m * ldc + c] = 0;
@@ -82,6 +87,8 @@ template <int DT>
 __global__ void __launch_bounds__(256) act_quant_row_kernel(
     const void* __restrict__ A, int64_t K, int64_t lda, int f16, int8_t* __restrict__ codes,
     int64_t ldc, float* __restrict__ scales, int32_t* err) {
+    griddep_wait();
+    griddep_launch();
     __shared__ float red[8];
     __shared__ int bad[8];
     const int64_t m = blockIdx.x;
@@ -115,30 +122,42 @@ __global__ void __launch_bounds__(256) act_quant_row_kernel(
     if (threadIdx.x == 0) scales[m] = s;
 }
 
+template <typename K, typename... Args>
+cudaError_t launch_ex(K kern, dim3 grid, dim3 block, bool pdl, cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 }  // namespace
 
 cudaError_t launch_act_quant(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda,
                              int group, int f16, int8_t* codes, int64_t ldc, float* scales,
-                             int32_t* err, cudaStream_t stream) {
+                             int64_t lds, int32_t* err, bool pdl, cudaStream_t stream) {
     if (M == 0) return cudaSuccess;
     if (group >= K) {
         const dim3 grid(static_cast<unsigned>(M));
         switch (a_dtype) {
-            case 0: act_quant_row_kernel<0><<<grid, 256, 0, stream>>>(A, K, lda, f16, codes, ldc, scales, err); break;
-            case 1: act_quant_row_kernel<1><<<grid, 256, 0, stream>>>(A, K, lda, f16, codes, ldc, scales, err); break;
-            default: act_quant_row_kernel<2><<<grid, 256, 0, stream>>>(A, K, lda, f16, codes, ldc, scales, err); break;
-        }
-    } else {
-        const int G = static_cast<int>((K + group - 1) / group);
-        const int64_t warps = M * G;
-        const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));
-        switch (a_dtype) {
-            case 0: act_quant_group_kernel<0><<<grid, 256, 0, stream>>>(A, M, K, lda, group, G, f16, codes, ldc, scales, err); break;
-            case 1: act_quant_group_kernel<1><<<grid, 256, 0, stream>>>(A, M, K, lda, group, G, f16, codes, ldc, scales, err); break;
-            default: act_quant_group_kernel<2><<<grid, 256, 0, stream>>>(A, M, K, lda, group, G, f16, codes, ldc, scales, err); break;
+            case 0: return launch_ex(act_quant_row_kernel<0>, grid, dim3(256), pdl, stream, A, K, lda, f16, codes, ldc, scales, err);
+            case 1: return launch_ex(act_quant_row_kernel<1>, grid, dim3(256), pdl, stream, A, K, lda, f16, codes, ldc, scales, err);
+            default: return launch_ex(act_quant_row_kernel<2>, grid, dim3(256), pdl, stream, A, K, lda, f16, codes, ldc, scales, err);
         }
     }
-    return cudaGetLastError();
+    const int G = static_cast<int>((K + group - 1) / group);
+    const int64_t warps = M * G;
+    const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));
+    switch (a_dtype) {
+        case 0: return launch_ex(act_quant_group_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, group, G, f16, codes, ldc, scales, lds, err);
+        case 1: return launch_ex(act_quant_group_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, group, G, f16, codes, ldc, scales, lds, err);
+        default: return launch_ex(act_quant_group_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, group, G, f16, codes, ldc, scales, lds, err);
+    }
 }
 
 }  // namespace mq

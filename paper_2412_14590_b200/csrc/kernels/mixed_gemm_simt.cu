@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128) mixed_gemm_simt_kernel(const GemmParams p
             if (mode == kFastToken) {
                 acc[t] = __fmaf_rn(gs, sw, acc[t]);
             } else {
-                const float sa = p.sa[m * p.sa_cols + (p.sa_cols == 1 ? 0 : g)];
+                const float sa = p.sa[int64_t(g) * p.sa_gstride + m];
                 acc[t] = __fadd_rn(acc[t], __fmul_rn(gs, __fmul_rn(sa, sw)));
             }
         }

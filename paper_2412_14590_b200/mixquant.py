@@ -234,8 +234,8 @@ def _stream(stream):
 
 
 def exec_opts(mode: int = capi.MQ_EXACT, act_group: int = 0, ksplit: int = 0, token_tile: int = 0,
-              gemm_impl: int = 0) -> capi.mq_exec_opts:
-    return capi.mq_exec_opts(mode, act_group, ksplit, token_tile, gemm_impl)
+              gemm_impl: int = 0, pdl: bool = True) -> capi.mq_exec_opts:
+    return capi.mq_exec_opts(mode, act_group, ksplit, token_tile, gemm_impl, 0 if pdl else 1)
 
 
 class DeviceLayer:
@@ -292,15 +292,17 @@ class DeviceLayer:
 
     def forward_codes(self, codes, scales, out=None, out_dtype=None, opts: capi.mq_exec_opts | None = None,
                       stream=None, workspace=None):
-        """execute_mixed_on_codes on device: codes int8 [M, ldc], scales f32."""
+        """execute_mixed_on_codes on device: codes int8 [M, ldc], scales f32
+        group-major [G, lds] (as quantize_act returns them)."""
         import torch
         opts = opts or exec_opts()
         M = codes.shape[0]
         if out is None:
             out = torch.empty((M, self.out_cols), dtype=out_dtype or torch.float32, device=codes.device)
         ws = workspace if workspace is not None else self.workspace(M, opts, False)
-        check(lib().mq_mixed_linear_codes(self.h, _p(codes), codes.stride(0), _p(scales), M, _p(out), _dt(out),
-                                          C.byref(opts), _p(ws), _stream(stream)))
+        lds = scales.stride(0) if scales.dim() == 2 else scales.numel()
+        check(lib().mq_mixed_linear_codes(self.h, _p(codes), codes.stride(0), _p(scales), lds, M, _p(out),
+                                          _dt(out), C.byref(opts), _p(ws), _stream(stream)))
         return out
 
     def partials(self, codes, which: int, stream=None):
@@ -314,15 +316,18 @@ class DeviceLayer:
 
 
 def quantize_act(A, group_size: int, ldc: int | None = None, err=None, stream=None):
-    """Activation quantization on device: returns (codes int8 [M, ldc], scales f32)."""
+    """Activation quantization on device: returns (codes int8 [M, ldc],
+    scales f32 group-major [G, lds]; G = 1 for per-token). scales[:, :M].T is
+    the reference's [M, G] array."""
     import torch
     M, K = A.shape
     ldc = ldc or (K + 127) // 128 * 128
     codes = torch.empty((M, ldc), dtype=torch.int8, device=A.device)
     G = 1 if group_size >= K else (K + group_size - 1) // group_size
-    scales = torch.empty((M, G), dtype=torch.float32, device=A.device)
-    check(lib().mq_quantize_act(_p(A), _dt(A), M, K, A.stride(0), group_size, _p(codes), ldc, _p(scales), _p(err),
-                                _stream(stream)))
+    lds = (M + 3) // 4 * 4
+    scales = torch.empty((G, lds), dtype=torch.float32, device=A.device)
+    check(lib().mq_quantize_act(_p(A), _dt(A), M, K, A.stride(0), group_size, _p(codes), ldc, _p(scales), lds,
+                                _p(err), _stream(stream)))
     return codes, scales
 
 
