@@ -212,21 +212,28 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
             const Seg sg = p.segs[si];
             const TileDesc td = p.tiles[sg.tile];
             for (int g = sg.g0; g < sg.g1; ++g, rs.next<NS>()) {
-                if (td.is8) continue;
                 ptx::mbar_wait(&full[rs.idx], rs.ph);
+                if (td.is8) {
+                    // keep conv[s] in lock-step with the ring (one phase per use
+                    // of the stage) even though sub8 stages need no conversion
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&conv[rs.idx]);
+                    continue;
+                }
                 uint8_t* st = stage(rs.idx);
                 const uint8_t* zp = st + C::kOffMeta + 512;
-                uint2 w[16];
-                uint32_t kk[16];
+                // 128 rows x 8 chunks of 16 codes = 1024 chunks: 8 per converter thread
+                uint2 w[8];
+                uint32_t kk[8];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < 8; ++i) {
                     const int q = i * 128 + ct, r = q >> 3, ch = q & 7;
                     w[i] = *reinterpret_cast<const uint2*>(st + r * 64 + ch * 8);
                     kk[i] = uint32_t(128 - zp[r]) * 0x01010101u;
                 }
                 named_bar_sync(4, 128);  // every raw byte read before any int8 byte lands
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
+                for (int i = 0; i < 8; ++i) {
                     const int q = i * 128 + ct, r = q >> 3, ch = q & 7;
                     uint4 o;
                     o.x = ((w[i].x & 0x0F0F0F0Fu) + kk[i]) ^ 0x80808080u;
