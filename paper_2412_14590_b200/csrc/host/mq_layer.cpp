@@ -1,6 +1,6 @@
 // mq_layer.cpp — device layer handle, the one-time packer into the engine's
-// HBM layout (mq_layout.cuh), the stream-K scheduler and the forward entry
-// points of the C ABI.
+// HBM layout (mq_layout.cuh), launch planning and the forward entry points of
+// the C ABI.
 //
 // The reference re-prepacks both sub-problems on every forward call
 // (proj/src/gemm.cpp:148-149, ~45% of its call time at M=16); here
@@ -12,8 +12,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
-#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -22,16 +22,6 @@
 #include "mq_internal.hpp"
 
 using namespace mq;
-
-namespace {
-struct Sched {
-    int grid = 0;
-    int slots = 0;        // stream-K partial tiles
-    int64_t items = 0;    // (tile, token block) work items
-    Seg* d_segs = nullptr;
-    int32_t* d_cta = nullptr;
-};
-}  // namespace
 
 struct mq_layer_s {
     int device = 0;
@@ -46,13 +36,11 @@ struct mq_layer_s {
     int64_t tiles8 = 0, tiles4 = 0;
     uint8_t* d_wq = nullptr;
     uint8_t* d_meta = nullptr;
-    TileDesc* d_tiles = nullptr;
     int32_t* d_colmap = nullptr;
     int64_t bytes_wq = 0, bytes_meta = 0, stream_bytes = 0;
-    std::vector<TileDesc> tiles;
+    std::vector<TileDesc> tiles;        // host copy (packing / accounting)
     std::vector<int32_t> shard_colmap;  // [world * shard_cols]
-    std::mutex mu;                      // guards the caches below
-    std::map<int64_t, Sched> scheds;    // keyed by (bn, token blocks, split)
+    std::mutex mu;                      // guards the internal workspace
     void* d_ws = nullptr;               // internal scratch (workspace = NULL)
     size_t ws_bytes = 0;
 };
@@ -87,101 +75,6 @@ int auto_token_tile(int64_t M) {
     return 128;
 }
 
-// ---------------------------------------------------------------- schedule
-// Weighted stream-K over work items (tile, token block) x K-groups: every CTA
-// gets ~1/P of the total streamed bytes (sub8 groups cost ~2x sub4 groups).
-// split=false (MQ_EXACT, dumps) keeps every item whole on one CTA so the
-// reference's ascending-group f32 accumulation order is preserved.
-void build_schedule(const std::vector<TileDesc>& tiles, int G, int bn, int tb, bool split, int sms,
-                    std::vector<Seg>& segs, std::vector<int32_t>& cta, int* slots) {
-    const int64_t T = static_cast<int64_t>(tiles.size());
-    auto gcost = [&](int64_t t) {
-        const TileDesc& td = tiles[t];
-        return double(td.copy_bytes + (td.is8 ? kMeta8Bytes : kMeta4Bytes)) + bn * 128.0 + 1024.0;
-    };
-    double total = 0;
-    for (int64_t t = 0; t < T; ++t) total += gcost(t) * G * tb;
-    const int64_t items = T * tb;
-    int P = sms;
-    if (!split) P = static_cast<int>(std::min<int64_t>(P, items));
-    else P = static_cast<int>(std::min<int64_t>(P, items * G));
-    P = std::max(P, 1);
-    const double target = total / P;
-    segs.clear();
-    cta.assign(1, 0);
-    double acc = 0;
-    int c = 0;
-    for (int64_t t = 0; t < T; ++t) {
-        const double gc = gcost(t);
-        for (int b = 0; b < tb; ++b) {
-            if (!split) {
-                segs.push_back(Seg{int32_t(t), b, 0, G, 1, 0, -1, 0});
-                acc += gc * G;
-                if (acc >= (c + 1) * target - 0.5 * gc && c < P - 1) {
-                    ++c;
-                    cta.push_back(static_cast<int32_t>(segs.size()));
-                }
-                continue;
-            }
-            int g = 0;
-            while (g < G) {
-                const double cap = (c + 1) * target - acc;
-                int k = static_cast<int>(std::floor(cap / gc + 0.5));
-                k = std::max(k, 1);
-                k = std::min(k, G - g);
-                if (G - g - k > 0 && G - g - k < 2) k = G - g;  // no 1-group tails
-                segs.push_back(Seg{int32_t(t), b, g, g + k, 1, 0, -1, 0});
-                acc += gc * k;
-                g += k;
-                if (acc >= (c + 1) * target - 0.5 * gc && c < P - 1) {
-                    ++c;
-                    cta.push_back(static_cast<int32_t>(segs.size()));
-                }
-            }
-        }
-    }
-    if (cta.back() != static_cast<int32_t>(segs.size())) cta.push_back(static_cast<int32_t>(segs.size()));
-    // segments of one item are contiguous: number them, give split ones slots
-    int s = 0;
-    for (size_t i = 0; i < segs.size();) {
-        size_t j = i;
-        while (j < segs.size() && segs[j].tile == segs[i].tile && segs[j].tb == segs[i].tb) ++j;
-        const int n = static_cast<int>(j - i);
-        for (size_t q = i; q < j; ++q) {
-            segs[q].nseg = n;
-            segs[q].sidx = static_cast<int32_t>(q - i);
-            segs[q].pslot = n > 1 ? s++ : -1;
-        }
-        i = j;
-    }
-    *slots = s;
-}
-
-mq_status get_sched(mq_layer_s* L, int bn, int tb, bool split, cudaStream_t stream, const Sched** out) {
-    const int64_t key = (int64_t(tb) << 16) | (int64_t(bn) << 1) | (split ? 1 : 0);
-    std::lock_guard<std::mutex> lk(L->mu);
-    auto it = L->scheds.find(key);
-    if (it != L->scheds.end()) {
-        *out = &it->second;
-        return MQ_OK;
-    }
-    cudaStreamCaptureStatus cs;
-    if (stream && cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
-        return fail(MQ_USAGE, "first forward of a (batch, mode) plan cannot be graph-captured; run it once eagerly");
-    std::vector<Seg> segs;
-    std::vector<int32_t> cta;
-    Sched sc;
-    build_schedule(L->tiles, L->G, bn, tb, split, L->num_sms, segs, cta, &sc.slots);
-    sc.grid = static_cast<int>(cta.size()) - 1;
-    sc.items = static_cast<int64_t>(L->tiles.size()) * tb;
-    CU_TRY(cudaMalloc(&sc.d_segs, std::max<size_t>(segs.size(), 1) * sizeof(Seg)));
-    CU_TRY(cudaMalloc(&sc.d_cta, cta.size() * sizeof(int32_t)));
-    CU_TRY(cudaMemcpy(sc.d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice));
-    CU_TRY(cudaMemcpy(sc.d_cta, cta.data(), cta.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    *out = &(L->scheds[key] = sc);
-    return MQ_OK;
-}
-
 struct Plan {
     int bn, tb, mode, per_token;
     bool split, pdl;
@@ -208,8 +101,23 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     return MQ_OK;
 }
 
-size_t ws_bytes_for(const Sched& sc, int bn) {
-    return ((size_t(sc.items) * 4 + 255) / 256) * 256 + size_t(sc.slots) * 128 * bn * 4;
+// The launch grid and the stream-K cost weights (bytes streamed per group,
+// incl. the activation tile and a fixed per-group pipeline cost).
+void fill_schedule(const mq_layer_s* L, const Plan& pl, int sms, GemmParams* p) {
+    const int64_t items = (L->tiles8 + L->tiles4) * pl.tb;
+    const int64_t X = items * L->G;
+    p->split = pl.split ? 1 : 0;
+    p->P = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(sms, pl.split ? X : items)));
+    p->c8 = (kCodes8Bytes + kMeta8Bytes + 128 * pl.bn + 1024) / 64;
+    p->c4 = (kCodes4Bytes + kMeta4Bytes + 128 * pl.bn + 1024) / 64;
+}
+
+size_t ws_bytes_for(const mq_layer_s* L, const Plan& pl, int sms) {
+    const int64_t items = (L->tiles8 + L->tiles4) * pl.tb;
+    const int64_t X = items * L->G;
+    const int64_t P = std::max<int64_t>(1, std::min<int64_t>(sms, pl.split ? X : items));
+    const size_t counters = ((size_t(items) * 4 + 255) / 256) * 256;
+    return counters + (pl.split ? size_t(2 * P) * 128 * pl.bn * 4 : 0);
 }
 
 mq_status encode_act_map(CUtensorMap* map, const int8_t* codes, int64_t ldc, int64_t M, int64_t K, int bn) {
@@ -226,12 +134,15 @@ mq_status encode_act_map(CUtensorMap* map, const int8_t* codes, int64_t ldc, int
     return MQ_OK;
 }
 
-void gemm_params(const mq_layer_s* L, const Plan& pl, const Sched* sc, const float* sa, int64_t lds, int64_t M,
-                 void* Y, mq_dtype out_dtype, void* ws, GemmParams* p) {
+void gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t lds, int64_t M, void* Y,
+                 mq_dtype out_dtype, void* ws, GemmParams* p) {
     std::memset(p, 0, sizeof(*p));
-    p->tiles = L->d_tiles;
-    p->num_tiles = static_cast<int32_t>(L->tiles8 + L->tiles4);
+    p->T8 = static_cast<int32_t>(L->tiles8);
+    p->T4 = static_cast<int32_t>(L->tiles4);
+    p->n8 = L->n8;
+    p->n4 = L->n4;
     p->G = L->G;
+    p->TB = pl.tb;
     p->K = L->K;
     p->wq = L->d_wq;
     p->wmeta = L->d_meta;
@@ -242,15 +153,19 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, const Sched* sc, const flo
     p->Y = Y;
     p->out_dtype = out_dtype;
     p->ldy = L->world > 1 ? L->shard_cols : L->N;
-    p->token_blocks = pl.tb;
-    if (sc) {
-        p->segs = sc->d_segs;
-        p->cta_seg = sc->d_cta;
+    fill_schedule(L, pl, L->num_sms, p);
+    if (ws) {
+        const int64_t items = (L->tiles8 + L->tiles4) * pl.tb;
         uint8_t* w = static_cast<uint8_t*>(ws);
         p->counters = reinterpret_cast<uint32_t*>(w);
-        p->ws = reinterpret_cast<float*>(w + ((size_t(sc->items) * 4 + 255) / 256) * 256);
+        p->ws = reinterpret_cast<float*>(w + ((size_t(items) * 4 + 255) / 256) * 256);
     }
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
+    static const int dbg = [] {
+        const char* e = std::getenv("MQ_DBG");
+        return e ? std::atoi(e) : 0;
+    }();
+    p->dbg = dbg;
 }
 
 mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, cudaStream_t stream, void** ws) {
@@ -417,7 +332,6 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     };
     cudaError_t e = upload(reinterpret_cast<void**>(&L->d_wq), wq.data(), size_t(L->bytes_wq));
     if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_meta), meta.data(), size_t(L->bytes_meta));
-    if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_tiles), L->tiles.data(), L->tiles.size() * sizeof(TileDesc));
     if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_colmap), colmap.data(), colmap.size() * 4);
     if (e != cudaSuccess) {
         mq_layer_destroy(L);
@@ -427,16 +341,12 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     return MQ_OK;
 }
 
+
 void mq_layer_destroy(mq_layer_t L) {
     if (!L) return;
     cudaFree(L->d_wq);
     cudaFree(L->d_meta);
-    cudaFree(L->d_tiles);
     cudaFree(L->d_colmap);
-    for (auto& kv : L->scheds) {
-        cudaFree(kv.second.d_segs);
-        cudaFree(kv.second.d_cta);
-    }
     if (L->d_ws) cudaFree(L->d_ws);
     delete L;
 }
@@ -481,9 +391,7 @@ mq_status mq_quantize_act(const void* A, mq_dtype dt, int64_t M, int64_t K, int6
 size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
     Plan pl;
     if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK) return 0;
-    const Sched* sc = nullptr;
-    if (get_sched(L, pl.bn, pl.tb, pl.split, nullptr, &sc) != MQ_OK) return 0;
-    return ws_bytes_for(*sc, pl.bn);
+    return ws_bytes_for(L, pl, L->num_sms);
 }
 
 mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, const float* scales, int64_t lds,
@@ -503,22 +411,21 @@ mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, 
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (o && o->gemm_impl == 1) {
         GemmParams p;
-        gemm_params(L, pl, nullptr, scales, lds, M, Y, out_dtype, nullptr, &p);
-        cudaError_t e = launch_mixed_gemm_simt(p, codes, ldc, pl.per_token && pl.mode == kFastToken ? kFastToken : kExactGroup,
+        gemm_params(L, pl, scales, lds, M, Y, out_dtype, nullptr, &p);
+        cudaError_t e = launch_mixed_gemm_simt(p, codes, ldc, pl.mode == kFastToken ? kFastToken : kExactGroup,
                                                L->w8_mode == MQ_W8_REFERENCE, s);
         if (e != cudaSuccess) return cuda_fail(e, "simt launch");
         return MQ_OK;
     }
-    const Sched* sc = nullptr;
-    if (mq_status st = get_sched(L, pl.bn, pl.tb, pl.split, s, &sc)) return st;
-    if (!ws && sc->slots > 0) {
-        if (mq_status st = ensure_internal_ws(L, ws_bytes_for(*sc, pl.bn), s, &ws)) return st;
+    const size_t need = ws_bytes_for(L, pl, L->num_sms);
+    if (!ws) {
+        if (mq_status st = ensure_internal_ws(L, need, s, &ws)) return st;
     }
     GemmParams p;
-    gemm_params(L, pl, sc, scales, lds, M, Y, out_dtype, ws, &p);
+    gemm_params(L, pl, scales, lds, M, Y, out_dtype, ws, &p);
     alignas(64) CUtensorMap map;
     if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
-    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, pl.mode, sc->grid, pl.pdl, s);
+    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, pl.mode, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
     return MQ_OK;
 }
@@ -558,39 +465,27 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
     if (M == 0) return MQ_OK;
     Plan pl;
     if (mq_status st = make_plan(L, M, nullptr, &pl)) return st;
-    const int64_t t0 = which == 0 ? 0 : L->tiles8;
-    const int64_t nt = which == 0 ? L->tiles8 : L->tiles4;
-    if (nt == 0) return MQ_OK;
-    // debug path: one whole item per CTA, schedule built per call
-    std::vector<TileDesc> sub(L->tiles.begin() + t0, L->tiles.begin() + t0 + nt);
-    std::vector<Seg> segs;
-    std::vector<int32_t> cta;
-    int slots = 0;
-    build_schedule(sub, L->G, pl.bn, pl.tb, false, 1 << 20, segs, cta, &slots);
-    Seg* d_segs = nullptr;
-    int32_t* d_cta = nullptr;
-    CU_TRY(cudaMalloc(&d_segs, segs.size() * sizeof(Seg)));
-    CU_TRY(cudaMalloc(&d_cta, cta.size() * sizeof(int32_t)));
-    CU_TRY(cudaMemcpy(d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice));
-    CU_TRY(cudaMemcpy(d_cta, cta.data(), cta.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    pl.split = false;
     GemmParams p;
-    gemm_params(L, pl, nullptr, nullptr, 0, M, nullptr, MQ_F32, nullptr, &p);
-    p.tiles = L->d_tiles + t0;
-    p.num_tiles = static_cast<int32_t>(nt);
-    p.segs = d_segs;
-    p.cta_seg = d_cta;
+    gemm_params(L, pl, nullptr, 0, M, nullptr, MQ_F32, nullptr, &p);
+    // restrict the launch to one sub-problem: its tiles, offsets and rows
+    if (which == 0) {
+        p.T4 = 0;
+        p.n4 = 0;
+    } else {
+        p.wq += L->tiles8 * L->G * kCodes8Bytes;
+        p.wmeta += L->tiles8 * L->G * kMeta8Bytes;
+        p.colmap += L->tiles8 * kTileRows;
+        p.T8 = 0;
+        p.n8 = 0;
+    }
+    if (p.T8 + p.T4 == 0) return MQ_OK;
+    p.P = static_cast<int32_t>(std::min<int64_t>(L->num_sms, int64_t(p.T8 + p.T4) * pl.tb));
     p.partials = partials;
     p.partial_rows = static_cast<int32_t>(which == 0 ? L->n8 : L->n4);
     alignas(64) CUtensorMap map;
-    mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn);
-    cudaError_t e = cudaSuccess;
-    if (st == MQ_OK)
-        e = launch_mixed_gemm_tc(p, &map, pl.bn, kDumpPartials, static_cast<int>(cta.size()) - 1, false,
-                                 static_cast<cudaStream_t>(stream));
-    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
-    cudaFree(d_segs);
-    cudaFree(d_cta);
-    if (st != MQ_OK) return st;
+    if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
+    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, kDumpPartials, false, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "partials launch");
     return MQ_OK;
 }

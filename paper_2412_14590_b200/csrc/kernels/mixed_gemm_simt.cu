@@ -22,7 +22,7 @@ __device__ __forceinline__ void store_out(void* Y, int dt, int64_t idx, float v)
 // grid (num_tiles, ceil(M/16)), block 128: thread = tile row.
 __global__ void __launch_bounds__(128) mixed_gemm_simt_kernel(const GemmParams p, const int8_t* __restrict__ codes,
                                                               int64_t ldc, int mode, int w8_unsigned) {
-    const TileDesc td = p.tiles[blockIdx.x];
+    const TileInfo td = tile_info(p, blockIdx.x);
     const int r = threadIdx.x;
     const int64_t m0 = int64_t(blockIdx.y) * kTok;
     if (r >= td.rows) return;
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(128) mixed_gemm_simt_kernel(const GemmParams p
             }
         }
     }
-    const int col = p.colmap[td.colmap_off + r];
+    const int col = p.colmap[blockIdx.x * kTileRows + r];
     for (int t = 0; t < kTok; ++t) {
         const int64_t m = m0 + t;
         if (m >= p.M) break;
@@ -105,8 +105,8 @@ __global__ void permute_kernel(const T* __restrict__ gathered, const int32_t* __
 
 cudaError_t launch_mixed_gemm_simt(const GemmParams& p, const int8_t* codes, int64_t ldc, int mode,
                                    int w8_unsigned, cudaStream_t stream) {
-    if (p.M == 0 || p.num_tiles == 0) return cudaSuccess;
-    const dim3 grid(p.num_tiles, static_cast<unsigned>((p.M + kTok - 1) / kTok));
+    if (p.M == 0 || p.T8 + p.T4 == 0) return cudaSuccess;
+    const dim3 grid(p.T8 + p.T4, static_cast<unsigned>((p.M + kTok - 1) / kTok));
     mixed_gemm_simt_kernel<<<grid, 128, 0, stream>>>(p, codes, ldc, mode, w8_unsigned);
     return cudaGetLastError();
 }

@@ -8,10 +8,12 @@
 // and the two sub-problems (8-bit / 4-bit output features) are scattered back
 // to their original columns (proj/src/mixed.cpp:83-120).
 //
-// B200 design: one persistent warp-specialised kernel over both sub-problems,
-// driven by a host-built stream-K schedule (Seg list per CTA):
+// B200 design: one persistent warp-specialised kernel over both sub-problems;
+// each CTA owns an arithmetically derived stream-K range of (tile, token
+// block, K-group) work (mq_kernels.hpp: Schedule), so the first weight copy
+// issues right after barrier init with no dependent global loads:
 //   warp 0      producer: cp.async.bulk of the packed weight codes + scales
-//               (L2 evict-first) — issued for the first NS stages BEFORE
+//               (L2 evict-first) — the first NS stages BEFORE
 //               griddepcontrol.wait so weight streaming overlaps the previous
 //               kernel under PDL — then a TMA 2-D tile of the int8 activations
 //               (SWIZZLE_128B) and the group's activation scales, NS-deep ring;
@@ -21,13 +23,13 @@
 //               paper's step-1 zero-point subtraction —
 //               written as the UMMA K-major SW128 image; sub8 tiles arrive
 //               pre-swizzled and skip it;
-//   warp 1      MMA issuer: 4 x tcgen05.mma (K = 32) per group into a fresh
-//               int32 TMEM accumulator (NACC-deep ring), tcgen05.commit
-//               releases the stage and signals the epilogue;
+//   warp 1      TMEM allocation, then MMA issue: 4 x tcgen05.mma (K = 32) per
+//               group into a fresh int32 TMEM accumulator (NACC-deep ring);
+//               tcgen05.commit releases the stage and signals the epilogue;
 //   warps 8..   epilogue: tcgen05.ld the group sums, exact int->float
 //               (I2FP), rescale and accumulate in f32 registers (step 2), then
 //               scatter the tile to the original output columns (f32/f16/bf16)
-//               or publish a stream-K partial.
+//               or publish a stream-K partial (last arriver reduces in order).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -86,22 +88,43 @@ struct Ring {
     }
 };
 
+// One contiguous run of K-groups of one work item inside this CTA's range.
+struct Seg {
+    int64_t x0;  // linear index of the first group
+    int64_t item;
+    int tile, tb, g0, g1;
+};
+__device__ __forceinline__ Seg seg_at(const GemmParams& p, int64_t x, int64_t xe) {
+    Seg s;
+    s.x0 = x;
+    s.item = x / p.G;
+    s.g0 = int(x - s.item * p.G);
+    const int64_t end = (s.item + 1) * p.G;
+    s.g1 = s.g0 + int((end < xe ? end : xe) - x);
+    s.tile = int(s.item / p.TB);
+    s.tb = int(s.item - int64_t(s.tile) * p.TB);
+    return s;
+}
+
 template <int BN, int MODE>
 __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1)
 mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmParams p) {
     using C = TcCfg<BN>;
     constexpr int NS = C::NS, NACC = C::NACC, NE = C::NE, BNE = C::BNE;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B aligned base (SWIZZLE_128B atoms), derived from smem_raw so the
+    // compiler keeps shared-space provenance (LDS/STS, not generic LD/ST)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stages = smem;
     uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * C::kStageBytes);
     uint64_t* full = bars;                 // [NS] producer (expect_tx)
-    uint64_t* conv = full + NS;            // [NS] converter -> MMA (sub4 stages)
+    uint64_t* conv = full + NS;            // [NS] converter -> MMA
     uint64_t* empty = conv + NS;           // [NS] MMA commit + epilogue warps
     uint64_t* tfull = empty + NS;          // [NACC] MMA commit -> epilogue
     uint64_t* tempty = tfull + NACC;       // [NACC] epilogue -> MMA
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + NACC);
-    volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_holder + 1);
+    uint64_t* tmem_ready = tempty + NACC;  // warp 1 -> epilogue
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_ready + 1);
+    int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto stage = [&](int s) { return stages + s * C::kStageBytes; };
@@ -116,74 +139,75 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 4 * NE);
         }
+        ptx::mbar_init(tmem_ready, 1);
         ptx::fence_barrier_init();
     }
-    if (warp == 1) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
-    if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_act);
-    ptx::tc_fence_before();
     __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
     griddep_launch();  // let the next kernel in the stream start its prologue
 
-    const int seg_lo = p.cta_seg[blockIdx.x], seg_hi = p.cta_seg[blockIdx.x + 1];
+    const Schedule S(p);
+    const int64_t xb = S.cut(blockIdx.x), xe = S.cut(blockIdx.x + 1);
 
     if (warp == 0) {
         // ============================== producer ==============================
         if (lane == 0) {
+            ptx::prefetch_tmap(&tmap_act);
             const uint64_t pol_w = ptx::policy_evict_first();
             const uint64_t pol_a = ptx::policy_evict_last();
             constexpr bool kSa = (MODE == kExactGroup || MODE == kFastGroup);
-            // pass 0 = weights of the first NS groups only (before the grid
-            // dependency resolves), pass 1 = everything else.
-            Ring ring;
-            int issued_w = 0;
+            const uint32_t b_bytes = (p.dbg & 8) ? 0u : uint32_t(C::kStageB);
+            // pass 0: weights of the first NS groups (independent of the
+            // previous kernel); pass 1: activations/scales + the rest.
             for (int pass = 0; pass < 2; ++pass) {
                 if (pass == 1) griddep_wait();
-                Ring rr;  // pass-local ring (pass 1 replays the prefetched stages)
+                Ring rr;
                 int n = 0;
-                for (int si = seg_lo; si < seg_hi; ++si) {
-                    const Seg sg = p.segs[si];
-                    const TileDesc td = p.tiles[sg.tile];
-                    const int cb = td.is8 ? kCodes8Bytes : kCodes4Bytes;
-                    const int mb = td.is8 ? kMeta8Bytes : kMeta4Bytes;
+                for (int64_t x = xb; x < xe && !(pass == 0 && n >= NS);) {
+                    const Seg sg = seg_at(p, x, xe);
+                    x += sg.g1 - sg.g0;
+                    const TileInfo ti = tile_info(p, sg.tile);
+                    const int cb = ti.is8 ? kCodes8Bytes : kCodes4Bytes;
+                    const int mb = ti.is8 ? kMeta8Bytes : kMeta4Bytes;
                     const int64_t m0 = int64_t(sg.tb) * BN;
                     const int64_t mrem = p.M - m0;
-                    const uint32_t sa_bytes = kSa ? uint32_t(((mrem < BN ? mrem : BN) + 3) / 4 * 16) : 0u;
+                    const uint32_t sa_bytes = kSa && !(p.dbg & 8) ? uint32_t(((mrem < BN ? mrem : BN) + 3) / 4 * 16) : 0u;
                     for (int g = sg.g0; g < sg.g1; ++g, ++n) {
-                        const bool pre = n < NS;  // prefetched in pass 0
+                        const bool pre = n < NS;
                         if (pass == 0 && !pre) break;
                         const int s = (pass == 0) ? n : rr.idx;
                         uint8_t* st = stage(s);
                         if (pass == 0 || !pre) {
                             if (pass == 1) ptx::mbar_wait(&empty[s], rr.ph ^ 1u);
-                            ptx::mbar_arrive_expect_tx(&full[s], td.copy_bytes + mb + C::kStageB + sa_bytes);
-                            ptx::bulk_g2s(st, p.wq + td.codes_off + int64_t(g) * cb, td.copy_bytes, &full[s], pol_w);
-                            ptx::bulk_g2s(st + C::kOffMeta, p.wmeta + td.meta_off + int64_t(g) * mb, mb, &full[s], pol_w);
-                            ++issued_w;
+                            ptx::mbar_arrive_expect_tx(&full[s], ti.copy_bytes + mb + b_bytes + sa_bytes);
+                            ptx::bulk_g2s(st, p.wq + ti.codes_off + int64_t(g) * cb, ti.copy_bytes, &full[s], pol_w);
+                            ptx::bulk_g2s(st + C::kOffMeta, p.wmeta + ti.meta_off + int64_t(g) * mb, mb, &full[s], pol_w);
                         }
                         if (pass == 1) {
-                            ptx::tma_load_2d(st + C::kOffB, &tmap_act, g * kGroupK, int32_t(m0), &full[s], pol_a);
-                            if constexpr (kSa)
+                            if (b_bytes) ptx::tma_load_2d(st + C::kOffB, &tmap_act, g * kGroupK, int32_t(m0), &full[s], pol_a);
+                            if (sa_bytes)
                                 ptx::bulk_g2s(st + C::kOffSa, p.sa + int64_t(g) * p.sa_gstride + m0, sa_bytes, &full[s], pol_a);
                             rr.next<NS>();
                         }
                     }
-                    if (pass == 0 && n >= NS) break;
                 }
             }
-            (void)ring;
-            (void)issued_w;
         }
     } else if (warp == 1) {
-        // ============================== MMA issuer ============================
+        // ======================= TMEM allocation + MMA issuer ==================
+        ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
+        ptx::tc_fence_before();
+        __syncwarp();
         if (lane == 0) {
+            ptx::mbar_arrive(tmem_ready);
+            ptx::tc_fence_after();
+            const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
             const uint32_t idesc4 = idesc_i8(BN, true, true);
             const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
             Ring rs, ra;
-            for (int si = seg_lo; si < seg_hi; ++si) {
-                const Seg sg = p.segs[si];
-                const bool is8 = p.tiles[sg.tile].is8 != 0;
+            for (int64_t x = xb; x < xe;) {
+                const Seg sg = seg_at(p, x, xe);
+                x += sg.g1 - sg.g0;
+                const bool is8 = sg.tile < p.T8;
                 const uint32_t idesc = is8 ? idesc8 : idesc4;
                 for (int g = sg.g0; g < sg.g1; ++g) {
                     ptx::mbar_wait(&tempty[ra.idx], ra.ph ^ 1u);
@@ -193,10 +217,12 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
                     const uint32_t a_addr = ptx::smem_u32(stage(rs.idx));
                     const uint32_t b_addr = a_addr + C::kOffB;
                     const uint32_t d_tmem = tmem_base + uint32_t(ra.idx * BN);
+                    if (!(p.dbg & 4)) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        ptx::mma_i8_ss(d_tmem, ptx::umma_desc_sw128(a_addr + 32 * k),
-                                       ptx::umma_desc_sw128(b_addr + 32 * k), idesc, k > 0);
+                        for (int k = 0; k < 4; ++k)
+                            ptx::mma_i8_ss(d_tmem, ptx::umma_desc_sw128(a_addr + 32 * k),
+                                           ptx::umma_desc_sw128(b_addr + 32 * k), idesc, k > 0);
+                    }
                     ptx::tc_commit(&tfull[ra.idx]);
                     ptx::tc_commit(&empty[rs.idx]);
                     rs.next<NS>();
@@ -208,12 +234,13 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
         // ====================== converter (in place, sub4) ====================
         const int ct = threadIdx.x - 128;
         Ring rs;
-        for (int si = seg_lo; si < seg_hi; ++si) {
-            const Seg sg = p.segs[si];
-            const TileDesc td = p.tiles[sg.tile];
+        for (int64_t x = xb; x < xe;) {
+            const Seg sg = seg_at(p, x, xe);
+            x += sg.g1 - sg.g0;
+            const bool is8 = sg.tile < p.T8;
             for (int g = sg.g0; g < sg.g1; ++g, rs.next<NS>()) {
                 ptx::mbar_wait(&full[rs.idx], rs.ph);
-                if (td.is8) {
+                if (is8 || (p.dbg & 2)) {
                     // keep conv[s] in lock-step with the ring (one phase per use
                     // of the stage) even though sub8 stages need no conversion
                     __syncwarp();
@@ -249,16 +276,21 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
         }
     } else if (warp >= 8) {
         // ============================== epilogue ==============================
-        griddep_wait();                    // workspace / scales of this launch are ours now
         const int et = threadIdx.x - 256;  // 0 .. 128*NE-1
         const int e = et >> 7;             // epilogue warpgroup
         const int wq = warp & 3;           // TMEM lane quarter this warp may access
         const int r = wq * 32 + lane;      // tile row (= TMEM lane)
         const int c0 = e * BNE;            // first token column of this warpgroup
+        ptx::mbar_wait(tmem_ready, 0);
+        ptx::tc_fence_after();
+        const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
+        griddep_wait();  // workspace / scales / output of this launch are ours now
         Ring rs, ra;
-        for (int si = seg_lo; si < seg_hi; ++si) {
-            const Seg sg = p.segs[si];
-            const TileDesc td = p.tiles[sg.tile];
+        for (int64_t x = xb; x < xe;) {
+            const Seg sg = seg_at(p, x, xe);
+            x += sg.g1 - sg.g0;
+            const TileInfo ti = tile_info(p, sg.tile);
+            const int col = r < ti.rows ? __ldg(p.colmap + sg.tile * kTileRows + r) : -1;  // prefetch
             const int64_t m0 = int64_t(sg.tb) * BN + c0;  // first token of this warpgroup
             float acc[BNE];
 #pragma unroll
@@ -272,16 +304,17 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
                 ptx::tc_fence_after();
 #pragma unroll
                 for (int ch = 0; ch < BNE / 16; ++ch) {
+                    if (p.dbg & 1) break;
                     uint32_t v[16];
                     ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + uint32_t(ra.idx * BN + c0 + ch * 16), v);
                     ptx::tmem_wait_ld();
                     if constexpr (MODE == kDumpPartials) {
-                        if (r < td.rows) {
+                        if (r < ti.rows) {
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
                                 const int64_t m = m0 + ch * 16 + j;
                                 if (m < p.M)
-                                    p.partials[(int64_t(g) * p.M + m) * p.partial_rows + td.sub_row0 + r] = int32_t(v[j]);
+                                    p.partials[(int64_t(g) * p.M + m) * p.partial_rows + ti.first + r] = int32_t(v[j]);
                             }
                         }
                     } else {
@@ -311,48 +344,50 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
             }
             if constexpr (MODE == kDumpPartials) continue;
 
-            const bool row_ok = r < td.rows;
-            const int col = row_ok ? __ldg(p.colmap + td.colmap_off + r) : -1;
             bool do_store = true;
-            if (sg.nseg > 1) {
-                // stream-K: publish this segment's partial tile; the last
-                // arriving segment sums the item's partials in sidx order.
-                const int64_t item = int64_t(sg.tile) * p.token_blocks + sg.tb;
-                float* part = p.ws + (int64_t(sg.pslot) * 128 + r) * BN + c0;
+            const int64_t xs = sg.item * p.G;  // the item's linear group range [xs, xs + G)
+            if (p.split && !(xb <= xs && xe >= xs + p.G)) {
+                // stream-K: this CTA holds only part of the item. Publish the
+                // partial tile to slot 2*c + (first segment of this CTA ? 0 : 1);
+                // the last arriving CTA sums the item's partials in CTA order.
+                const int c = blockIdx.x;
+                const int slot = 2 * c + (sg.x0 == xb ? 0 : 1);
+                float* part = p.ws + (int64_t(slot) * 128 + r) * BN + c0;
 #pragma unroll
                 for (int j = 0; j < BNE; j += 4)
                     __stcg(reinterpret_cast<float4*>(part + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
                 __threadfence();
                 named_bar_sync(3, 128 * NE);
+                const int ca = S.cta_of(xs), cz = S.cta_of(xs + p.G - 1);
                 if (et == 0) {
-                    const uint32_t prev = atomicAdd(p.counters + item, 1u);
-                    *last_flag = (prev == uint32_t(sg.nseg - 1));
+                    const uint32_t prev = atomicAdd(p.counters + sg.item, 1u);
+                    *reinterpret_cast<volatile int*>(last_flag) = (prev == uint32_t(cz - ca));
                 }
                 named_bar_sync(3, 128 * NE);
-                do_store = *last_flag != 0;
+                do_store = *reinterpret_cast<volatile int*>(last_flag) != 0;
                 if (do_store) {
                     __threadfence();
-                    const float* base = p.ws + (int64_t(sg.pslot - sg.sidx) * 128 + r) * BN + c0;
-#pragma unroll
-                    for (int j = 0; j < BNE; j += 4) {
-                        const float4 t = __ldcg(reinterpret_cast<const float4*>(base + j));
-                        acc[j] = t.x; acc[j + 1] = t.y; acc[j + 2] = t.z; acc[j + 3] = t.w;
-                    }
-                    for (int k = 1; k < sg.nseg; ++k) {
-                        const float* b2 = base + int64_t(k) * 128 * BN;
+                    const bool ca_first = S.cut(ca) == xs;
+                    for (int k = ca; k <= cz; ++k) {
+                        const int sk = 2 * k + ((k == ca && !ca_first) ? 1 : 0);
+                        const float* src = p.ws + (int64_t(sk) * 128 + r) * BN + c0;
 #pragma unroll
                         for (int j = 0; j < BNE; j += 4) {
-                            const float4 t = __ldcg(reinterpret_cast<const float4*>(b2 + j));
-                            acc[j] = __fadd_rn(acc[j], t.x);
-                            acc[j + 1] = __fadd_rn(acc[j + 1], t.y);
-                            acc[j + 2] = __fadd_rn(acc[j + 2], t.z);
-                            acc[j + 3] = __fadd_rn(acc[j + 3], t.w);
+                            const float4 t = __ldcg(reinterpret_cast<const float4*>(src + j));
+                            if (k == ca) {
+                                acc[j] = t.x; acc[j + 1] = t.y; acc[j + 2] = t.z; acc[j + 3] = t.w;
+                            } else {
+                                acc[j] = __fadd_rn(acc[j], t.x);
+                                acc[j + 1] = __fadd_rn(acc[j + 1], t.y);
+                                acc[j + 2] = __fadd_rn(acc[j + 2], t.z);
+                                acc[j + 3] = __fadd_rn(acc[j + 3], t.w);
+                            }
                         }
                     }
-                    if (et == 0) p.counters[item] = 0u;  // re-arm for the next launch
+                    if (et == 0) p.counters[sg.item] = 0u;  // re-arm for the next launch
                 }
             }
-            if (do_store && row_ok) {
+            if (do_store && col >= 0) {
 #pragma unroll
                 for (int j = 0; j < BNE; ++j) {
                     const int64_t m = m0 + j;
@@ -370,12 +405,12 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const GemmPar
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+        ptx::tmem_dealloc<C::kTmemCols>(*reinterpret_cast<volatile uint32_t*>(tmem_holder));
     }
 }
 
 template <int BN, int MODE>
-cudaError_t launch_bn_mode(const GemmParams& p, const void* tmap, int grid, bool pdl, cudaStream_t stream) {
+cudaError_t launch_bn_mode(const GemmParams& p, const void* tmap, bool pdl, cudaStream_t stream) {
     using C = TcCfg<BN>;
     auto kern = mixed_gemm_tc_kernel<BN, MODE>;
     static thread_local uint64_t configured = 0;  // per device ordinal bitmask
@@ -386,9 +421,9 @@ cudaError_t launch_bn_mode(const GemmParams& p, const void* tmap, int grid, bool
         if (e != cudaSuccess) return e;
         configured |= uint64_t(1) << dev;
     }
-    if (grid <= 0) return cudaSuccess;
+    if (p.P <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = dim3(p.P);
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = stream;
@@ -401,12 +436,12 @@ cudaError_t launch_bn_mode(const GemmParams& p, const void* tmap, int grid, bool
 }
 
 template <int BN>
-cudaError_t launch_bn(const GemmParams& p, const void* tmap, int mode, int grid, bool pdl, cudaStream_t s) {
+cudaError_t launch_bn(const GemmParams& p, const void* tmap, int mode, bool pdl, cudaStream_t s) {
     switch (mode) {
-        case kExactGroup: return launch_bn_mode<BN, kExactGroup>(p, tmap, grid, pdl, s);
-        case kFastGroup: return launch_bn_mode<BN, kFastGroup>(p, tmap, grid, pdl, s);
-        case kFastToken: return launch_bn_mode<BN, kFastToken>(p, tmap, grid, pdl, s);
-        default: return launch_bn_mode<BN, kDumpPartials>(p, tmap, grid, pdl, s);
+        case kExactGroup: return launch_bn_mode<BN, kExactGroup>(p, tmap, pdl, s);
+        case kFastGroup: return launch_bn_mode<BN, kFastGroup>(p, tmap, pdl, s);
+        case kFastToken: return launch_bn_mode<BN, kFastToken>(p, tmap, pdl, s);
+        default: return launch_bn_mode<BN, kDumpPartials>(p, tmap, pdl, s);
     }
 }
 
@@ -421,13 +456,13 @@ int gemm_stages(int bn) {
     }
 }
 
-cudaError_t launch_mixed_gemm_tc(const GemmParams& p, const void* tmap, int token_tile, int mode, int grid,
-                                 bool pdl, cudaStream_t stream) {
+cudaError_t launch_mixed_gemm_tc(const GemmParams& p, const void* tmap, int token_tile, int mode, bool pdl,
+                                 cudaStream_t stream) {
     switch (token_tile) {
-        case 16: return launch_bn<16>(p, tmap, mode, grid, pdl, stream);
-        case 32: return launch_bn<32>(p, tmap, mode, grid, pdl, stream);
-        case 64: return launch_bn<64>(p, tmap, mode, grid, pdl, stream);
-        case 128: return launch_bn<128>(p, tmap, mode, grid, pdl, stream);
+        case 16: return launch_bn<16>(p, tmap, mode, pdl, stream);
+        case 32: return launch_bn<32>(p, tmap, mode, pdl, stream);
+        case 64: return launch_bn<64>(p, tmap, mode, pdl, stream);
+        case 128: return launch_bn<128>(p, tmap, mode, pdl, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -256,7 +256,10 @@ class DeviceLayer:
     def __del__(self):
         h = getattr(self, "h", None)
         if h:
-            lib().mq_layer_destroy(h)
+            try:
+                lib().mq_layer_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already gone
+                pass
             self.h = None
 
     @property
