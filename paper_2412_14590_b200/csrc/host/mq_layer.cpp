@@ -35,9 +35,8 @@ struct mq_layer_s {
     int w8_mode = MQ_W8_REFERENCE;
     int64_t tiles8 = 0, tiles4 = 0;
     uint8_t* d_wq = nullptr;
-    uint8_t* d_meta = nullptr;
     int32_t* d_colmap = nullptr;
-    int64_t bytes_wq = 0, bytes_meta = 0, stream_bytes = 0;
+    int64_t bytes_wq = 0, stream_bytes = 0;
     std::vector<TileDesc> tiles;        // host copy (packing / accounting)
     std::vector<int32_t> shard_colmap;  // [world * shard_cols]
     std::mutex mu;                      // guards the internal workspace
@@ -46,6 +45,8 @@ struct mq_layer_s {
 };
 
 namespace {
+
+unsigned long long* g_trace_buf = nullptr;
 
 mq_status cuda_fail(cudaError_t e, const char* what) {
     return fail(MQ_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -101,15 +102,21 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     return MQ_OK;
 }
 
+void fill_cuts(GemmParams* p) {
+    const Schedule S(*p);
+    for (int c = 0; c <= p->P; ++c) p->cuts[c] = static_cast<int32_t>(S.cut(c));
+}
+
 // The launch grid and the stream-K cost weights (bytes streamed per group,
 // incl. the activation tile and a fixed per-group pipeline cost).
 void fill_schedule(const mq_layer_s* L, const Plan& pl, int sms, GemmParams* p) {
     const int64_t items = (L->tiles8 + L->tiles4) * pl.tb;
     const int64_t X = items * L->G;
     p->split = pl.split ? 1 : 0;
-    p->P = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(sms, pl.split ? X : items)));
-    p->c8 = (kCodes8Bytes + kMeta8Bytes + 128 * pl.bn + 1024) / 64;
-    p->c4 = (kCodes4Bytes + kMeta4Bytes + 128 * pl.bn + 1024) / 64;
+    p->P = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>({int64_t(sms), int64_t(kMaxCtas), pl.split ? X : items})));
+    p->c8 = (kBlock8Bytes + 128 * pl.bn + 1024) / 64;
+    p->c4 = (kBlock4Bytes + 128 * pl.bn + 1024) / 64;
+    fill_cuts(p);
 }
 
 size_t ws_bytes_for(const mq_layer_s* L, const Plan& pl, int sms) {
@@ -120,17 +127,35 @@ size_t ws_bytes_for(const mq_layer_s* L, const Plan& pl, int sms) {
     return counters + (pl.split ? size_t(2 * P) * 128 * pl.bn * 4 : 0);
 }
 
-mq_status encode_act_map(CUtensorMap* map, const int8_t* codes, int64_t ldc, int64_t M, int64_t K, int bn) {
+// Activation codes as a 3-D tensor {128 (k in group), M, G} with byte strides
+// {ldc, 128}: one box {128, BN, GPS} lands GPS per-group [BN][128] SW128 tiles.
+// Scales (group-major [G][lds] f32) as 2-D {M, G}: box {BN, GPS}.
+mq_status encode_maps(CUtensorMap* amap, CUtensorMap* smap, const int8_t* codes, int64_t ldc, const float* scales,
+                      int64_t lds, int64_t M, int G, int bn, bool with_scales) {
     auto fn = encode_fn();
     if (!fn) return fail(MQ_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc)};
-    const cuuint32_t box[2] = {128u, static_cast<cuuint32_t>(bn)};
-    const cuuint32_t estr[2] = {1u, 1u};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(codes), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(MQ_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    const int gps = gemm_gps(bn);
+    {
+        const cuuint64_t dims[3] = {128u, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(G)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldc), 128u};
+        const cuuint32_t box[3] = {128u, static_cast<cuuint32_t>(bn), static_cast<cuuint32_t>(gps)};
+        const cuuint32_t estr[3] = {1u, 1u, 1u};
+        CUresult r = fn(amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(codes), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(MQ_CUDA, "cuTensorMapEncodeTiled(codes) failed: " + std::to_string(int(r)));
+    }
+    std::memset(smap, 0, sizeof(*smap));
+    if (with_scales) {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(G)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(lds) * 4u};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(bn), static_cast<cuuint32_t>(gps)};
+        const cuuint32_t estr[2] = {1u, 1u};
+        CUresult r = fn(smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(scales), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(MQ_CUDA, "cuTensorMapEncodeTiled(scales) failed: " + std::to_string(int(r)));
+    }
     return MQ_OK;
 }
 
@@ -145,7 +170,6 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t l
     p->TB = pl.tb;
     p->K = L->K;
     p->wq = L->d_wq;
-    p->wmeta = L->d_meta;
     p->colmap = L->d_colmap;
     p->sa = sa;
     p->sa_gstride = pl.per_token ? 0 : lds;
@@ -166,6 +190,16 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t l
         return e ? std::atoi(e) : 0;
     }();
     p->dbg = dbg;
+    if (dbg & 32) {
+        static unsigned long long* tr = [] {
+            unsigned long long* t = nullptr;
+            cudaMalloc(&t, 148 * 8 * sizeof(unsigned long long));
+            cudaMemset(t, 0, 148 * 8 * sizeof(unsigned long long));
+            return t;
+        }();
+        p->trace = tr;
+        g_trace_buf = tr;
+    }
 }
 
 mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, cudaStream_t stream, void** ws) {
@@ -262,13 +296,11 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
 
     // ---- pack (host), then upload once
     const int64_t T = L->tiles8 + L->tiles4;
-    L->bytes_wq = (L->tiles8 * kCodes8Bytes + L->tiles4 * kCodes4Bytes) * G;
-    L->bytes_meta = (L->tiles8 * kMeta8Bytes + L->tiles4 * kMeta4Bytes) * G;
+    L->bytes_wq = (L->tiles8 * kBlock8Bytes + L->tiles4 * kBlock4Bytes) * G;
     std::vector<uint8_t> wq(size_t(std::max<int64_t>(L->bytes_wq, 1)), 0);
-    std::vector<uint8_t> meta(size_t(std::max<int64_t>(L->bytes_meta, 1)), 0);
     std::vector<int32_t> colmap(size_t(std::max<int64_t>(T * kTileRows, 1)), -1);
     L->tiles.resize(size_t(T));
-    int64_t coff = 0, moff = 0;
+    int64_t coff = 0;
     const int64_t stride4 = row_stride(4, K);
     for (int64_t t = 0; t < T; ++t) {
         const bool is8 = t < L->tiles8;
@@ -277,12 +309,9 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
         const int rows = static_cast<int>(std::min<int64_t>(kTileRows, nloc - first));
         TileDesc& td = L->tiles[t];
         td.codes_off = coff;
-        td.meta_off = moff;
         td.is8 = is8;
         td.rows = rows;
-        td.colmap_off = static_cast<int32_t>(t * kTileRows);
-        td.copy_bytes = is8 ? ((rows + 7) / 8) * 1024 : rows * 64;
-        td.sub_row0 = static_cast<int32_t>(first);
+        td.first = static_cast<int32_t>(first);
         td.pad = 0;
         for (int r = 0; r < rows; ++r) {
             const int64_t srow = (is8 ? a8 : a4) + first + r;  // global sub-problem row
@@ -292,8 +321,8 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
         }
         for (int64_t g = 0; g < G; ++g) {
             const int64_t k0 = g * kGroupK;
-            uint8_t* cb = wq.data() + coff + g * (is8 ? kCodes8Bytes : kCodes4Bytes);
-            uint8_t* mb = meta.data() + moff + g * (is8 ? kMeta8Bytes : kMeta4Bytes);
+            uint8_t* cb = wq.data() + coff + g * (is8 ? kBlock8Bytes : kBlock4Bytes);
+            uint8_t* mb = cb + (is8 ? kCodes8Bytes : kCodes4Bytes);  // scales | zero points
             for (int r = 0; r < rows; ++r) {
                 const int64_t srow = (is8 ? a8 : a4) + first + r;
                 float sc;
@@ -320,9 +349,8 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
                 std::memcpy(mb + 4 * r, &sc, 4);
             }
         }
-        coff += (is8 ? kCodes8Bytes : kCodes4Bytes) * G;
-        moff += (is8 ? kMeta8Bytes : kMeta4Bytes) * G;
-        L->stream_bytes += int64_t(td.copy_bytes + (is8 ? kMeta8Bytes : kMeta4Bytes)) * G;
+        coff += (is8 ? kBlock8Bytes : kBlock4Bytes) * G;
+        L->stream_bytes += int64_t(is8 ? kBlock8Bytes : kBlock4Bytes) * G;
     }
 
     auto upload = [&](void** dst, const void* src, size_t n) -> cudaError_t {
@@ -331,7 +359,6 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
         return n ? cudaMemcpy(*dst, src, n, cudaMemcpyHostToDevice) : cudaSuccess;
     };
     cudaError_t e = upload(reinterpret_cast<void**>(&L->d_wq), wq.data(), size_t(L->bytes_wq));
-    if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_meta), meta.data(), size_t(L->bytes_meta));
     if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_colmap), colmap.data(), colmap.size() * 4);
     if (e != cudaSuccess) {
         mq_layer_destroy(L);
@@ -345,7 +372,6 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
 void mq_layer_destroy(mq_layer_t L) {
     if (!L) return;
     cudaFree(L->d_wq);
-    cudaFree(L->d_meta);
     cudaFree(L->d_colmap);
     if (L->d_ws) cudaFree(L->d_ws);
     delete L;
@@ -360,7 +386,7 @@ mq_status mq_layer_get_info(mq_layer_t L, mq_layer_info* info) {
     info->n4 = L->n4;
     info->tiles8 = L->tiles8;
     info->tiles4 = L->tiles4;
-    info->device_bytes = L->bytes_wq + L->bytes_meta;
+    info->device_bytes = L->bytes_wq;
     info->weight_stream_bytes = L->stream_bytes;
     info->rank = L->rank;
     info->world = L->world;
@@ -400,7 +426,8 @@ mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, 
     if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
     if (M == 0) return MQ_OK;
-    if (ldc < L->K || ldc % 16 != 0) return fail(MQ_USAGE, "ldc must be >= K and a multiple of 16 (TMA row pitch)");
+    if (ldc < int64_t(L->G) * kGroupK || ldc % 16 != 0)
+        return fail(MQ_USAGE, "ldc must be >= ceil(K/128)*128 (zero-padded columns) and a multiple of 16");
     if (reinterpret_cast<uintptr_t>(codes) % 16 != 0) return fail(MQ_USAGE, "codes must be 16-byte aligned");
     if (reinterpret_cast<uintptr_t>(scales) % 16 != 0) return fail(MQ_USAGE, "scales must be 16-byte aligned");
     if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
@@ -423,9 +450,9 @@ mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, 
     }
     GemmParams p;
     gemm_params(L, pl, scales, lds, M, Y, out_dtype, ws, &p);
-    alignas(64) CUtensorMap map;
-    if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
-    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, pl.mode, pl.pdl, s);
+    alignas(64) CUtensorMap amap, smap;
+    if (mq_status st = encode_maps(&amap, &smap, codes, ldc, scales, lds, M, L->G, pl.bn, !pl.per_token)) return st;
+    cudaError_t e = launch_mixed_gemm_tc(p, &amap, &smap, pl.bn, pl.mode, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
     return MQ_OK;
 }
@@ -461,7 +488,8 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
                            void* stream) {
     if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (which != 0 && which != 1) return fail(MQ_USAGE, "which must be 0 (sub8) or 1 (sub4)");
-    if (ldc < L->K || ldc % 16 != 0) return fail(MQ_USAGE, "ldc must be >= K and a multiple of 16");
+    if (ldc < int64_t(L->G) * kGroupK || ldc % 16 != 0)
+        return fail(MQ_USAGE, "ldc must be >= ceil(K/128)*128 (zero-padded columns) and a multiple of 16");
     if (M == 0) return MQ_OK;
     Plan pl;
     if (mq_status st = make_plan(L, M, nullptr, &pl)) return st;
@@ -473,21 +501,29 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
         p.T4 = 0;
         p.n4 = 0;
     } else {
-        p.wq += L->tiles8 * L->G * kCodes8Bytes;
-        p.wmeta += L->tiles8 * L->G * kMeta8Bytes;
+        p.wq += L->tiles8 * L->G * kBlock8Bytes;
         p.colmap += L->tiles8 * kTileRows;
         p.T8 = 0;
         p.n8 = 0;
     }
     if (p.T8 + p.T4 == 0) return MQ_OK;
-    p.P = static_cast<int32_t>(std::min<int64_t>(L->num_sms, int64_t(p.T8 + p.T4) * pl.tb));
+    p.P = static_cast<int32_t>(std::min<int64_t>({int64_t(L->num_sms), int64_t(kMaxCtas), int64_t(p.T8 + p.T4) * pl.tb}));
+    fill_cuts(&p);
     p.partials = partials;
     p.partial_rows = static_cast<int32_t>(which == 0 ? L->n8 : L->n4);
-    alignas(64) CUtensorMap map;
-    if (mq_status st = encode_act_map(&map, codes, ldc, M, L->K, pl.bn)) return st;
-    cudaError_t e = launch_mixed_gemm_tc(p, &map, pl.bn, kDumpPartials, false, static_cast<cudaStream_t>(stream));
+    alignas(64) CUtensorMap amap, smap;
+    if (mq_status st = encode_maps(&amap, &smap, codes, ldc, nullptr, 0, M, L->G, pl.bn, false)) return st;
+    cudaError_t e = launch_mixed_gemm_tc(p, &amap, &smap, pl.bn, kDumpPartials, false, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "partials launch");
     return MQ_OK;
+}
+
+// development: copy the last traced launch's per-CTA timestamps (MQ_DBG & 32)
+int mq_debug_trace(unsigned long long* out) {
+    if (!g_trace_buf) return 0;
+    cudaDeviceSynchronize();
+    cudaMemcpy(out, g_trace_buf, 148 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    return 148;
 }
 
 mq_status mq_permute_gathered(const void* gathered, const int32_t* colmap, int32_t world, int64_t sc, int64_t M,

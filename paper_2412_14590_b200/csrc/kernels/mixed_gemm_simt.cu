@@ -26,14 +26,13 @@ __global__ void __launch_bounds__(128) mixed_gemm_simt_kernel(const GemmParams p
     const int r = threadIdx.x;
     const int64_t m0 = int64_t(blockIdx.y) * kTok;
     if (r >= td.rows) return;
-    const int cb = td.is8 ? kCodes8Bytes : kCodes4Bytes;
-    const int mb = td.is8 ? kMeta8Bytes : kMeta4Bytes;
+    const int cb = td.blk;
     float acc[kTok];
 #pragma unroll
     for (int t = 0; t < kTok; ++t) acc[t] = 0.0f;
     for (int g = 0; g < p.G; ++g) {
-        const uint8_t* blk = p.wq + td.codes_off + int64_t(g) * cb;
-        const uint8_t* meta = p.wmeta + td.meta_off + int64_t(g) * mb;
+        const uint8_t* blk = p.wq + td.off + int64_t(g) * cb;
+        const uint8_t* meta = blk + (td.is8 ? kCodes8Bytes : kCodes4Bytes);
         const float sw = reinterpret_cast<const float*>(meta)[r];
         const int z = td.is8 ? 0 : meta[512 + r];
         int32_t s[kTok];

@@ -21,14 +21,15 @@ enum GemmMode : int {
 // K-groups, linearised item-major with the sub8 tiles first; CTA c owns the
 // linear group range [cut(c), cut(c+1)) — cost-weighted (sub8 groups stream
 // ~2x the bytes of sub4 groups) when split, whole items otherwise.
+constexpr int kMaxCtas = 160;  // >= SM count (148 on B200)
+
 struct GemmParams {
     int32_t T8, T4;         // 128-row tiles of sub8 / sub4
     int64_t n8, n4;         // rows of sub8 / sub4
     int32_t G;              // K-groups
     int32_t TB;             // token blocks (BN tokens each)
     int64_t K;
-    const uint8_t* wq;      // codes blocks (mq_layout.cuh)
-    const uint8_t* wmeta;   // meta blocks
+    const uint8_t* wq;      // merged code+meta blocks (mq_layout.cuh)
     const int32_t* colmap;  // [ (T8+T4)*128 ] output column of every tile row
     const float* sa;        // activation scales, group-major: sa[g * sa_gstride + m]
     int64_t sa_gstride;     // lds (group-wise) or 0 (per-token)
@@ -44,14 +45,20 @@ struct GemmParams {
     uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int32_t* partials;      // dump mode
     int32_t partial_rows;
+    int32_t cuts[kMaxCtas + 1];  // CTA c owns linear groups [cuts[c], cuts[c+1]) (param space: no loads)
     int32_t dbg;            // development: pipeline-stage bypass bits (MQ_DBG env), 0 in production
+    unsigned long long* trace;  // development: per-CTA globaltimer stamps [P][8] (MQ_DBG & 32)
 };
 
 // tcgen05 product kernel. token_tile in {16,32,64,128}; mode per GemmMode;
+// tmap_act: 3-D tensor map {128, M, G} over the int8 codes (box {128, BN, GPS});
+// tmap_sa: 2-D tensor map {M, G} over the group-major scales (box {BN, GPS});
 // pdl = launch with programmatic stream serialization (prologue + weight
 // prefetch overlap the previous kernel).
-cudaError_t launch_mixed_gemm_tc(const GemmParams& p, const void* tmap_act, int token_tile, int mode,
-                                 bool pdl, cudaStream_t stream);
+cudaError_t launch_mixed_gemm_tc(const GemmParams& p, const void* tmap_act, const void* tmap_sa, int token_tile,
+                                 int mode, bool pdl, cudaStream_t stream);
+// groups of a sub4 tile per pipeline stage (sub8: half) for a token tile
+constexpr int gemm_gps(int token_tile) { return token_tile <= 32 ? 4 : 2; }
 int gemm_stages(int token_tile);
 // SIMT debug kernel (same layout, exact op order); parity aid, not the product.
 cudaError_t launch_mixed_gemm_simt(const GemmParams& p, const int8_t* codes, int64_t ldc,
@@ -66,8 +73,8 @@ cudaError_t launch_permute(const void* gathered, const int32_t* colmap, int worl
 
 // Tile descriptor of tile t (sub8 tiles first), identical to the host packer.
 struct TileInfo {
-    int64_t codes_off, meta_off;
-    int32_t is8, rows, copy_bytes, first;
+    int64_t off;     // byte offset of the tile's group-0 block
+    int32_t is8, rows, first, blk;
 };
 __host__ __device__ inline TileInfo tile_info(const GemmParams& p, int t) {
     TileInfo ti;
@@ -75,24 +82,34 @@ __host__ __device__ inline TileInfo tile_info(const GemmParams& p, int t) {
     const int64_t G = p.G;
     if (ti.is8) {
         ti.first = t * kTileRows;
-        ti.codes_off = int64_t(t) * G * kCodes8Bytes;
-        ti.meta_off = int64_t(t) * G * kMeta8Bytes;
+        ti.off = int64_t(t) * G * kBlock8Bytes;
+        ti.blk = kBlock8Bytes;
         const int64_t rem = p.n8 - ti.first;
         ti.rows = int32_t(rem < kTileRows ? rem : kTileRows);
-        ti.copy_bytes = (ti.rows + 7) / 8 * 1024;
     } else {
         const int u = t - p.T8;
         ti.first = u * kTileRows;
-        ti.codes_off = int64_t(p.T8) * G * kCodes8Bytes + int64_t(u) * G * kCodes4Bytes;
-        ti.meta_off = int64_t(p.T8) * G * kMeta8Bytes + int64_t(u) * G * kMeta4Bytes;
+        ti.off = int64_t(p.T8) * G * kBlock8Bytes + int64_t(u) * G * kBlock4Bytes;
+        ti.blk = kBlock4Bytes;
         const int64_t rem = p.n4 - ti.first;
         ti.rows = int32_t(rem < kTileRows ? rem : kTileRows);
-        ti.copy_bytes = ti.rows * 64;
     }
     return ti;
 }
 
-// The stream-K partition (see GemmParams).
+// CTA owning linear group x (binary search over the parameter-space cut table).
+__host__ __device__ inline int cta_owner(const GemmParams& p, int32_t x) {
+    int lo = 0, hi = p.P - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p.cuts[mid] <= x) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// The stream-K partition (see GemmParams); evaluated once on the host to fill
+// GemmParams::cuts.
 struct Schedule {
     int64_t X8, X, U, items;
     int32_t G, P, split, c8, c4;

@@ -2,17 +2,20 @@
 // the host packer (mq_layer.cpp) and the sm_100a kernels.
 //
 // A layer is cut into 128-row TILES (tcgen05 M = 128): first the sub8 tiles,
-// then the sub4 tiles. For every (tile, K-group of 128) there is one CODES
-// block and one META block, stored tile-major / group-minor so a CTA working
-// on a tile streams one contiguous range with cp.async.bulk:
-//   sub8 codes block  16384 B: 128 rows x 128 int8, already in the UMMA
-//                     K-major SWIZZLE_128B image (copied straight to smem and
-//                     consumed by tcgen05.mma, no conversion);
-//   sub4 codes block   8192 B: 128 rows x 64 B of nibbles, row r / 16-code
-//                     chunk c at r*64 + c*8, nibble order chosen so the
-//                     converter's output words are byte-ordered (see below);
-//   meta block         512 B f32 scales[128] (+ 128 B u8 zero points for sub4).
-// Ragged tiles copy only the valid rows (rows rounded to 8 for sub8).
+// then the sub4 tiles. For every (tile, K-group of 128) there is one BLOCK
+// holding the group's codes followed by its metadata, stored tile-major /
+// group-minor, so a run of consecutive groups of one tile is ONE contiguous
+// range the producer moves with a single cp.async.bulk (on sm_100a the bulk
+// copy engine is bounded per operation, not per byte: few, large copies):
+//   sub8 block 17408 B: codes 16384 B = 128 rows x 128 int8 already in the
+//              UMMA K-major SWIZZLE_128B image (consumed by tcgen05.mma in
+//              place, no conversion) | f32 scales[128] | 512 B pad (keeps every
+//              block 1024-B aligned for the SW128 atoms);
+//   sub4 block  8832 B: codes 8192 B = 128 rows x 64 B of nibbles, row r /
+//              16-code chunk c at r*64 + c*8, nibble order chosen so the
+//              converter's output words are byte-ordered (see pack_chunk4) |
+//              f32 scales[128] | u8 zero points[128].
+// Rows past the end of a ragged tile are zero.
 #pragma once
 #include <cstdint>
 
@@ -22,20 +25,16 @@ constexpr int kTileRows = 128;      // tcgen05.mma M
 constexpr int kGroupK = 128;        // K-group = one SWIZZLE_128B atom row of int8
 constexpr int kCodes8Bytes = 16384; // 128 x 128 int8
 constexpr int kCodes4Bytes = 8192;  // 128 x 128 nibbles
-constexpr int kMeta8Bytes = 512;
-constexpr int kMeta4Bytes = 640;
+constexpr int kBlock8Bytes = 17408; // codes | scales | pad
+constexpr int kBlock4Bytes = 8832;  // codes | scales | zero points
 
-struct TileDesc {
-    int64_t codes_off;   // byte offset of the tile's group-0 codes block
-    int64_t meta_off;    // byte offset of the tile's group-0 meta block
+struct TileDesc {  // host-side bookkeeping of one tile
+    int64_t codes_off;   // byte offset of the tile's group-0 block
     int32_t is8;         // 1: sub8 tile (int8 codes), 0: sub4 tile (u4 + zero points)
     int32_t rows;        // valid rows in the tile (1..128)
-    int32_t colmap_off;  // index of the tile's row 0 in the column map
-    int32_t copy_bytes;  // codes bytes per group to stream (valid rows only)
-    int32_t sub_row0;    // first sub-problem row of the tile (debug dumps)
+    int32_t first;       // first sub-problem row of the tile
     int32_t pad;
 };
-static_assert(sizeof(TileDesc) == 40, "TileDesc is 40 bytes");
 
 // Byte offset of int8 element (row r, k) inside a 128-row K-major
 // SWIZZLE_128B image: 8-row x 128 B atoms, 16-byte chunks XOR-ed by r%8.

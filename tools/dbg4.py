@@ -1,0 +1,27 @@
+import sys, os, ctypes as C
+sys.path.insert(0, "/root/repo")
+import numpy as np, torch
+import paper_2412_14590_b200 as mq
+from paper_2412_14590_b200 import capi
+N, K, M = (int(x) for x in sys.argv[1:4])
+W, A, prom = mq.bench_inputs(M, N, K, 0.1, 1)
+L = mq.partition_and_quantize(W, prom)
+dl = mq.DeviceLayer(L)
+dA = torch.from_numpy(A).cuda()
+codes, scales = mq.quantize_act(dA, 128)
+Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
+opts = mq.exec_opts(capi.MQ_FAST, 128, pdl=False)
+for _ in range(3): dl.forward_codes(codes, scales, out=Y, opts=opts)
+torch.cuda.synchronize()
+t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+t0.record(); dl.forward_codes(codes, scales, out=Y, opts=opts); t1.record(); torch.cuda.synchronize()
+print("event us", t0.elapsed_time(t1) * 1e3)
+buf = (C.c_ulonglong * (148 * 8))()
+n = capi.lib().mq_debug_trace(buf)
+a = np.array(buf, dtype=np.float64).reshape(148, 8)
+base = a[:, 0][a[:, 0] > 0].min()
+a = np.where(a > 0, a - base, np.nan) / 1000.0
+names = ["start", "prod_pass1", "prod_after_gdw", "epi_first_tfull", "epi_seg_done", "epi_exit", "end"]
+for i, nm in enumerate(names):
+    col = a[:, i]
+    print(f"{nm:16s} min {np.nanmin(col):7.2f} med {np.nanmedian(col):7.2f} max {np.nanmax(col):7.2f} us")
