@@ -193,8 +193,8 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t l
     if (dbg & 32) {
         static unsigned long long* tr = [] {
             unsigned long long* t = nullptr;
-            cudaMalloc(&t, 148 * 8 * sizeof(unsigned long long));
-            cudaMemset(t, 0, 148 * 8 * sizeof(unsigned long long));
+            cudaMalloc(&t, (148 * 8 + 1024) * sizeof(unsigned long long));
+            cudaMemset(t, 0, (148 * 8 + 1024) * sizeof(unsigned long long));
             return t;
         }();
         p->trace = tr;
@@ -340,8 +340,8 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
                         }
                         uint32_t w0, w1;
                         pack_chunk4(e, &w0, &w1);
-                        std::memcpy(cb + r * 64 + ch * 8, &w0, 4);
-                        std::memcpy(cb + r * 64 + ch * 8 + 4, &w1, 4);
+                        std::memcpy(cb + sub4_chunk_offset(r, ch), &w0, 4);
+                        std::memcpy(cb + sub4_chunk_offset(r, ch) + 4, &w1, 4);
                     }
                     sc = d->scales4[srow * G + g];
                     mb[512 + r] = d->zero_points4[srow * G + g];
@@ -522,7 +522,7 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
 int mq_debug_trace(unsigned long long* out) {
     if (!g_trace_buf) return 0;
     cudaDeviceSynchronize();
-    cudaMemcpy(out, g_trace_buf, 148 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(out, g_trace_buf, (148 * 8 + 1024) * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     return 148;
 }
 

@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(128) mixed_gemm_simt_kernel(const GemmParams p
                     wv[j] = w8_unsigned ? int(b) : int(int8_t(b));
                 }
             } else {
-                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(blk + r * 64 + ch * 8);
-                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(blk + r * 64 + ch * 8 + 4);
+                const uint32_t w0 = *reinterpret_cast<const uint32_t*>(blk + sub4_chunk_offset(r, ch));
+                const uint32_t w1 = *reinterpret_cast<const uint32_t*>(blk + sub4_chunk_offset(r, ch) + 4);
                 for (int j = 0; j < 4; ++j) {
                     wv[j] = int((w0 >> (8 * j)) & 15u) - z;
                     wv[4 + j] = int((w0 >> (8 * j + 4)) & 15u) - z;

@@ -10,26 +10,28 @@
 //
 // B200 design: one persistent warp-specialised kernel over both sub-problems;
 // CTA c owns the stream-K range [cuts[c], cuts[c+1]) of linearised
-// (tile, token block, K-group) work (mq_kernels.hpp). The bulk-copy engine is
-// bounded per operation, so a pipeline STAGE carries a CHUNK of up to GPS
-// consecutive groups of one tile (GPS/2 for sub8) and is filled by three
-// copies: one cp.async.bulk of the merged code+meta blocks (L2 evict-first),
-// one 3-D TMA of the chunk's int8 activation tiles (SWIZZLE_128B) and one 2-D
-// TMA of its activation scales.
-//   warp 0      producer; the first NS weight copies issue BEFORE
-//               griddepcontrol.wait, so under PDL weight streaming overlaps
-//               the previous kernel;
-//   warps 4-7   converter (sub4): nibbles -> int8 (c - z) with the carry-free
-//               bias trick ((x & 0x0F0F0F0F) + (128 - z)*0x01010101) ^ 0x80808080
-//               — the paper's step-1 zero-point subtraction
-//               — into a CR-deep ring of UMMA K-major SW128 images; sub8 blocks
-//               are consumed in place;
-//   warp 1      TMEM allocation, then MMA issue: 4 x tcgen05.mma (K = 32) per
-//               group into a fresh int32 TMEM accumulator (NACC-deep ring);
-//   warps 8..   epilogue: tcgen05.ld the group sums, exact int->float
-//               (I2FP), rescale and accumulate in f32 registers (step 2), then
-//               scatter the tile to the original output columns (f32/f16/bf16)
-//               or publish a stream-K partial (last arriver reduces in order).
+// (tile, token block, K-group) work (mq_kernels.hpp). Work moves in CHUNKS of
+// up to GPS consecutive groups of one tile (GPS/2 for sub8); every hand-off
+// between roles is per chunk, not per group (mbarrier round trips dominate
+// at decode sizes):
+//   warp 0      producer: per chunk one cp.async.bulk of the merged code+meta
+//               blocks (L2 evict-first), one 3-D TMA of the chunk's int8
+//               activation tiles (SWIZZLE_128B), one 2-D TMA of its activation
+//               scales; the first NS weight copies issue BEFORE
+//               griddepcontrol.wait so under PDL they overlap the previous kernel;
+//   converter   (sub4) one thread per weight row: 4 conflict-free 16-B loads,
+//               nibbles -> int8 (c - z) with the carry-free bias trick
+//               ((x & 0x0F0F0F0F) + (128 - z)*0x01010101) ^ 0x80808080 — the
+//               paper's step-1 zero-point subtraction — and a
+//               tcgen05.st of the row straight into a TMEM A-operand ring;
+//   warp 1      TMEM allocation, then MMA issue (elected lane): 4 x tcgen05.mma
+//               (K = 32) per group, A from TMEM (sub4) or from the
+//               pre-swizzled SMEM block (sub8), each group into a fresh int32
+//               TMEM accumulator;
+//   epilogue    tcgen05.ld the group sums, exact int->float (I2FP), rescale and
+//               accumulate in f32 registers (step 2), then scatter the tile to
+//               the original output columns (f32/f16/bf16) or publish a
+//               stream-K partial (last arriver reduces in fixed order).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -44,29 +46,39 @@ constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 
 template <int BN>
 struct TcCfg {
-    static constexpr int GPS = gemm_gps(BN);                // sub4 groups per stage
-    static constexpr int GPS8 = GPS / 2 > 0 ? GPS / 2 : 1;  // sub8 groups per stage
+    static constexpr int GPS = gemm_gps(BN);                // sub4 groups per chunk
+    static constexpr int GPS8 = GPS / 2 > 0 ? GPS / 2 : 1;  // sub8 groups per chunk
     static constexpr int kRaw0 = GPS * kBlock4Bytes > GPS8 * kBlock8Bytes ? GPS * kBlock4Bytes : GPS8 * kBlock8Bytes;
     static constexpr int kRaw = (kRaw0 + 1023) / 1024 * 1024;
     static constexpr int kOffB = kRaw;                     // [GPS][BN][128] int8, SW128
     static constexpr int kOffSa = kOffB + GPS * BN * 128;  // [GPS][BN] f32
     static constexpr int kStageBytes = ((kOffSa + GPS * BN * 4) + 1023) / 1024 * 1024;
-    static constexpr int CR = 3;                           // conversion ring (16 KB images)
-    static constexpr int kConv = CR * kCodes8Bytes;
     static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/;
-    static constexpr int NS0 = (kSmemMax - kFixed - kConv) / kStageBytes;
+    static constexpr int NS0 = (kSmemMax - kFixed) / kStageBytes;
     static constexpr int NS = NS0 > 8 ? 8 : NS0;
-    static constexpr int NACC = BN <= 32 ? 8 : 4;  // TMEM accumulator ring
-    static constexpr uint32_t kTmemCols = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128 : (NACC * BN <= 256) ? 256 : 512;
+    static constexpr int NCS = 2;                            // chunk slots of the TMEM rings
+    static constexpr uint32_t kAccCols = NCS * GPS * BN;     // int32 accumulators
+    static constexpr uint32_t kACol0 = kAccCols;             // A ring: NCS*GPS tiles x 32 cols
+    static constexpr uint32_t kTmemNeed = kAccCols + NCS * GPS * 32;
+    static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
+    static_assert(kTmemNeed <= 512, "TMEM budget");
     static constexpr int NE = BN <= 64 ? 1 : 2;  // epilogue warpgroups
+    static constexpr int NC = BN <= 32 ? 2 : 1;  // converter warpgroups (decode is conversion-bound)
     static constexpr int BNE = BN / NE;          // tokens per epilogue warpgroup
-    static constexpr int kThreads = 128 * (2 + NE);
-    static constexpr int kSmem = kFixed + kConv + NS * kStageBytes;
+    static constexpr int kEpiThread0 = 128 * (1 + NC);
+    static constexpr int kThreads = 128 * (1 + NC + NE);
+    static constexpr int kSmem = kFixed + NS * kStageBytes;
     static_assert(NS >= 2, "pipeline needs at least two stages");
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// one lane of a converged warp (elect.sync): keeps tcgen05/TMA operands warp-uniform
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
 }
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -77,6 +89,11 @@ __device__ __forceinline__ void trace(const GemmParams& p, int ev) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[blockIdx.x * 8 + ev] = t;
     }
+}
+// per-chunk event trace of one CTA (MQ_DBG & 64, CTA = MQ_DBG >> 8), in SM cycles
+__device__ __forceinline__ void trace_chunk(const GemmParams& p, int ev, int n) {
+    if (p.trace && (p.dbg & 64) && int(blockIdx.x) == (p.dbg >> 8) && n < 64)
+        p.trace[148 * 8 + ev * 64 + n] = clock64();
 }
 
 __device__ __forceinline__ void store_out(void* Y, int dt, int64_t idx, float v) {
@@ -116,27 +133,32 @@ __device__ __forceinline__ Seg seg_at(const GemmParams& p, int32_t x, int32_t xe
     return s;
 }
 
+// nibbles of one packed word -> two words of int8 (c - z): codes 0..3 and 4..7
+__device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& lo, uint32_t& hi) {
+    lo = ((w & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
+    hi = (((w >> 4) & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
+}
+
 template <int BN, int MODE>
 __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1)
 mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_constant__ CUtensorMap tmap_sa,
                      const __grid_constant__ GemmParams p) {
     using C = TcCfg<BN>;
-    constexpr int NS = C::NS, NACC = C::NACC, NE = C::NE, BNE = C::BNE, GPS = C::GPS, CR = C::CR;
+    constexpr int NS = C::NS, NE = C::NE, BNE = C::BNE, GPS = C::GPS, NCS = C::NCS, NC = C::NC;
     constexpr bool kSa = (MODE == kExactGroup || MODE == kFastGroup);
     extern __shared__ uint8_t smem_raw[];
     // 1024-B aligned base (SWIZZLE_128B atoms), derived from smem_raw so the
     // compiler keeps shared-space provenance (LDS/STS, not generic LD/ST)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* conv = smem;               // [CR][16384]
-    uint8_t* stages = smem + C::kConv;  // [NS][kStageBytes]
+    uint8_t* stages = smem;  // [NS][kStageBytes]
     uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * C::kStageBytes);
     uint64_t* full = bars;                 // [NS] producer (expect_tx)
-    uint64_t* empty = full + NS;           // [NS] MMA commit + epilogue warps (per chunk)
-    uint64_t* cfull = empty + NS;          // [CR] converter -> MMA
-    uint64_t* cempty = cfull + CR;         // [CR] MMA commit -> converter
-    uint64_t* tfull = cempty + CR;         // [NACC] MMA commit -> epilogue
-    uint64_t* tempty = tfull + NACC;       // [NACC] epilogue -> MMA
-    uint64_t* tmem_ready = tempty + NACC;  // warp 1 -> epilogue
+    uint64_t* empty = full + NS;           // [NS] MMA commit + epilogue warps
+    uint64_t* afull = empty + NS;          // [NCS] converter -> MMA (TMEM A tiles written)
+    uint64_t* aempty = afull + NCS;        // [NCS] MMA commit -> converter
+    uint64_t* tfull = aempty + NCS;        // [NCS] MMA commit -> epilogue
+    uint64_t* tempty = tfull + NCS;        // [NCS] epilogue -> MMA
+    uint64_t* tmem_ready = tempty + NCS;   // warp 1 -> everyone using TMEM
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_ready + 1);
     int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
@@ -148,11 +170,9 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1 + 4 * NE);
         }
-        for (int i = 0; i < CR; ++i) {
-            ptx::mbar_init(&cfull[i], 4);
-            ptx::mbar_init(&cempty[i], 1);
-        }
-        for (int i = 0; i < NACC; ++i) {
+        for (int i = 0; i < NCS; ++i) {
+            ptx::mbar_init(&afull[i], 4 * NC);
+            ptx::mbar_init(&aempty[i], 1);
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 4 * NE);
         }
@@ -182,160 +202,175 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
 
     if (warp == 0) {
         // ============================== producer ==============================
-        if (lane == 0) {
+        if (elect_one()) {
             ptx::prefetch_tmap(&tmap_act);
             if (kSa) ptx::prefetch_tmap(&tmap_sa);
-            const uint64_t pol_w = ptx::policy_evict_first();
-            const uint64_t pol_a = ptx::policy_evict_last();
-            constexpr uint32_t kBBytes = GPS * BN * 128;  // full boxes (OOB rows / groups zero-filled)
-            constexpr uint32_t kSaBytes = kSa ? GPS * BN * 4 : 0;
-            // pass 0: weights of the first NS chunks (independent of the previous
-            // kernel); pass 1: activations/scales + everything else.
-            for (int pass = 0; pass < 2; ++pass) {
-                if (pass == 1) {
-                    trace(p, 1);
-                    griddep_wait();
-                    trace(p, 2);
-                }
-                Ring rr;
-                int n = 0;
-                for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
-                    const bool pre = n < NS;
-                    if (pass == 0 && !pre) return false;
-                    uint8_t* st = stage(rr.idx);
-                    if (pass == 0 || !pre) {
-                        if (pass == 1) ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
-                        const uint32_t wbytes = uint32_t(cg * ti.blk);
+        }
+        const uint64_t pol_w = ptx::policy_evict_first();
+        const uint64_t pol_a = ptx::policy_evict_last();
+        constexpr uint32_t kBBytes = GPS * BN * 128;  // full boxes (OOB rows / groups zero-filled)
+        constexpr uint32_t kSaBytes = kSa ? GPS * BN * 4 : 0;
+        // pass 0: weights of the first NS chunks (independent of the previous
+        // kernel); pass 1: activations/scales + everything else.
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 1) {
+                if (lane == 0) trace(p, 1);
+                griddep_wait();
+                if (lane == 0) trace(p, 2);
+            }
+            Ring rr;
+            int n = 0;
+            for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
+                const bool pre = n < NS;
+                if (pass == 0 && !pre) return false;
+                uint8_t* st = stage(rr.idx);
+                if (pass == 0 || !pre) {
+                    if (pass == 1) ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
+                    if (lane == 0) trace_chunk(p, 0, n);
+                    const uint32_t wbytes = uint32_t(cg * ti.blk);
+                    if (elect_one()) {
                         ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes + kBBytes + kSaBytes);
                         ptx::bulk_g2s(st, p.wq + ti.off + int64_t(gc) * ti.blk, wbytes, &full[rr.idx], pol_w);
                     }
-                    if (pass == 1) {
+                    __syncwarp();
+                }
+                if (pass == 1) {
+                    if (elect_one()) {
                         ptx::tma_load_3d(st + C::kOffB, &tmap_act, 0, sg.tb * BN, gc, &full[rr.idx], pol_a);
                         if (kSa) ptx::tma_load_2d(st + C::kOffSa, &tmap_sa, sg.tb * BN, gc, &full[rr.idx], pol_a);
                     }
-                    rr.next<NS>();
-                    ++n;
-                    return true;
-                });
-            }
+                    __syncwarp();
+                }
+                rr.next<NS>();
+                ++n;
+                return true;
+            });
         }
     } else if (warp == 1) {
         // ======================= TMEM allocation + MMA issuer ==================
         ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-            ptx::mbar_arrive(tmem_ready);
-            ptx::tc_fence_after();
-            const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
-            const uint32_t idesc4 = idesc_i8(BN, true, true);
-            const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
-            Ring rs, rc, ra;
-            for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
-                ptx::mbar_wait(&full[rs.idx], rs.ph);
-                const uint32_t st = ptx::smem_u32(stage(rs.idx));
-                for (int j = 0; j < cg; ++j) {
-                    uint32_t a_addr;
-                    if (ti.is8) {
-                        a_addr = st + j * kBlock8Bytes;
-                    } else {
-                        ptx::mbar_wait(&cfull[rc.idx], rc.ph);
-                        a_addr = ptx::smem_u32(conv + rc.idx * kCodes8Bytes);
-                    }
-                    ptx::mbar_wait(&tempty[ra.idx], ra.ph ^ 1u);
-                    ptx::tc_fence_after();
-                    const uint32_t b_addr = st + C::kOffB + j * (BN * 128);
-                    const uint32_t d_tmem = tmem_base + uint32_t(ra.idx * BN);
-                    const uint32_t idesc = ti.is8 ? idesc8 : idesc4;
-                    if (!(p.dbg & 4)) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            ptx::mma_i8_ss(d_tmem, ptx::umma_desc_sw128(a_addr + 32 * k),
-                                           ptx::umma_desc_sw128(b_addr + 32 * k), idesc, k > 0);
-                    }
-                    ptx::tc_commit(&tfull[ra.idx]);
-                    if (!ti.is8) {
-                        ptx::tc_commit(&cempty[rc.idx]);
-                        rc.next<CR>();
-                    }
-                    ra.next<NACC>();
-                }
-                ptx::tc_commit(&empty[rs.idx]);
-                rs.next<NS>();
-                return true;
-            });
-        }
-    } else if (warp >= 4 && warp < 8) {
-        // ======================= converter (sub4 -> int8 image) ==================
-        const int ct = threadIdx.x - 128;
-        Ring rs, rc;
+        if (lane == 0) ptx::mbar_arrive(tmem_ready);
+        ptx::tc_fence_after();
+        const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
+        const uint32_t idesc4 = idesc_i8(BN, true, true);
+        const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
+        Ring rs, ra, rt;
+        int nch = 0;
         for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
-            if (!ti.is8) {
-                ptx::mbar_wait(&full[rs.idx], rs.ph);
-                const uint8_t* st = stage(rs.idx);
-                for (int j = 0; j < cg; ++j) {
-                    ptx::mbar_wait(&cempty[rc.idx], rc.ph ^ 1u);
-                    const uint8_t* raw = st + j * kBlock4Bytes;
-                    const uint8_t* zp = raw + kCodes4Bytes + 512;
-                    uint8_t* dst = conv + rc.idx * kCodes8Bytes;
-                    if (!(p.dbg & 2)) {
-                        // 128 rows x 8 chunks of 16 codes = 1024 chunks: 8 per thread
+            ptx::mbar_wait(&full[rs.idx], rs.ph);
+            if (!ti.is8) ptx::mbar_wait(&afull[ra.idx], ra.ph);
+            ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
+            ptx::tc_fence_after();
+            if (lane == 0) trace_chunk(p, 1, nch);
+            const uint32_t st = ptx::smem_u32(stage(rs.idx));
+            if (elect_one()) {
+                if (!(p.dbg & 4)) {
+                    for (int j = 0; j < cg; ++j) {
+                        const uint32_t d_tmem = tmem_base + uint32_t((rt.idx * GPS + j) * BN);
+                        const uint32_t b_addr = st + C::kOffB + j * (BN * 128);
+                        if (ti.is8) {
+                            const uint32_t a_addr = st + j * kBlock8Bytes;
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int q = i * 128 + ct, r = q >> 3, ch = q & 7;
-                            const uint2 w = *reinterpret_cast<const uint2*>(raw + r * 64 + ch * 8);
-                            const uint32_t kk = uint32_t(128 - zp[r]) * 0x01010101u;
-                            uint4 o;
-                            o.x = ((w.x & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
-                            o.y = (((w.x >> 4) & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
-                            o.z = ((w.y & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
-                            o.w = (((w.y >> 4) & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
-                            *reinterpret_cast<uint4*>(dst + (r >> 3) * 1024 + (r & 7) * 128 + ((ch ^ (r & 7)) << 4)) = o;
+                            for (int k = 0; k < 4; ++k)
+                                ptx::mma_i8_ss(d_tmem, ptx::umma_desc_sw128(a_addr + 32 * k),
+                                               ptx::umma_desc_sw128(b_addr + 32 * k), idesc8, k > 0);
+                        } else {
+                            const uint32_t a_tmem = tmem_base + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                ptx::mma_i8_ts(d_tmem, a_tmem + 8 * k, ptx::umma_desc_sw128(b_addr + 32 * k), idesc4,
+                                               k > 0);
                         }
                     }
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&cfull[rc.idx]);
-                    rc.next<CR>();
                 }
+                ptx::tc_commit(&tfull[rt.idx]);
+                if (!ti.is8) ptx::tc_commit(&aempty[ra.idx]);
+                ptx::tc_commit(&empty[rs.idx]);
             }
+            __syncwarp();
+            if (lane == 0) trace_chunk(p, 2, nch++);
+            if (!ti.is8) ra.next<NCS>();
+            rt.next<NCS>();
             rs.next<NS>();
             return true;
         });
-    } else if (warp >= 8) {
+    } else if (warp >= 4 && warp < 4 + 4 * NC) {
+        // =================== converter (sub4 -> int8 A tiles in TMEM) ===================
+        const int wg = (warp - 4) >> 2;   // converter warpgroup: takes groups j = wg, wg+NC, ...
+        const int r = (warp & 3) * 32 + lane;  // weight row = TMEM lane
+        ptx::mbar_wait(tmem_ready, 0);
+        ptx::tc_fence_after();
+        const uint32_t tmem_row = *reinterpret_cast<volatile uint32_t*>(tmem_holder) + (uint32_t((warp & 3) * 32) << 16);
+        Ring rs, ra;
+        int nch = 0;
+        for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
+            if (!ti.is8) {
+                ptx::mbar_wait(&full[rs.idx], rs.ph);
+                ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
+                const uint8_t* st = stage(rs.idx);
+                for (int j = wg; j < cg; j += NC) {
+                    const uint8_t* raw = st + j * kBlock4Bytes;
+                    const uint32_t kk = uint32_t(128 - raw[kCodes4Bytes + 512 + r]) * 0x01010101u;
+                    uint32_t v[32];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 w = *reinterpret_cast<const uint4*>(raw + q * 2048 + r * 16);
+                        unpack_word(w.x, kk, v[q * 8 + 0], v[q * 8 + 1]);
+                        unpack_word(w.y, kk, v[q * 8 + 2], v[q * 8 + 3]);
+                        unpack_word(w.z, kk, v[q * 8 + 4], v[q * 8 + 5]);
+                        unpack_word(w.w, kk, v[q * 8 + 6], v[q * 8 + 7]);
+                    }
+                    if (!(p.dbg & 2)) ptx::tmem_st32(tmem_row + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32), v);
+                }
+                ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&afull[ra.idx]);
+                ra.next<NCS>();
+            }
+            if (threadIdx.x == 128) trace_chunk(p, 3, nch);
+            ++nch;
+            rs.next<NS>();
+            return true;
+        });
+    } else {
         // ============================== epilogue ==============================
-        const int et = threadIdx.x - 256;  // 0 .. 128*NE-1
-        const int e = et >> 7;             // epilogue warpgroup
-        const int wq = warp & 3;           // TMEM lane quarter this warp may access
-        const int r = wq * 32 + lane;      // tile row (= TMEM lane)
-        const int c0 = e * BNE;            // first token column of this warpgroup
+        const int et = threadIdx.x - C::kEpiThread0;  // 0 .. 128*NE-1
+        const int e = et >> 7;                        // epilogue warpgroup
+        const int wq = warp & 3;                      // TMEM lane quarter this warp may access
+        const int r = wq * 32 + lane;                 // tile row (= TMEM lane)
+        const int c0 = e * BNE;                       // first token column of this warpgroup
         ptx::mbar_wait(tmem_ready, 0);
         ptx::tc_fence_after();
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
         griddep_wait();  // workspace / scales / output of this launch are ours now
-        Ring rs, ra;
+        Ring rs, rt;
         bool first_group = true;
         float acc[BNE];
+        int nch = 0;
         for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
             if (gc == sg.g0) {
 #pragma unroll
                 for (int j = 0; j < BNE; ++j) acc[j] = 0.0f;
             }
             ptx::mbar_wait(&full[rs.idx], rs.ph);
+            ptx::mbar_wait(&tfull[rt.idx], rt.ph);
+            ptx::tc_fence_after();
+            if (first_group && et == 0) trace(p, 3);
+            first_group = false;
             const uint8_t* st = stage(rs.idx);
             const int64_t m0 = int64_t(sg.tb) * BN + c0;  // first token of this warpgroup
             for (int j = 0; j < cg; ++j) {
                 const float sw = reinterpret_cast<const float*>(st + j * ti.blk + (ti.is8 ? kCodes8Bytes : kCodes4Bytes))[r];
                 const float* sav = reinterpret_cast<const float*>(st + C::kOffSa) + j * BN + c0;
-                ptx::mbar_wait(&tfull[ra.idx], ra.ph);
-                ptx::tc_fence_after();
-                if (first_group && et == 0) trace(p, 3);
-                first_group = false;
+                const uint32_t tcol = uint32_t((rt.idx * GPS + j) * BN + c0);
 #pragma unroll
                 for (int ch = 0; ch < BNE / 16; ++ch) {
                     if (p.dbg & 1) break;
                     uint32_t v[16];
-                    ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + uint32_t(ra.idx * BN + c0 + ch * 16), v);
+                    ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * 16, v);
                     ptx::tmem_wait_ld();
                     if constexpr (MODE == kDumpPartials) {
                         if (r < ti.rows) {
@@ -362,13 +397,16 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                         }
                     }
                 }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[ra.idx]);
-                ra.next<NACC>();
             }
+            ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&empty[rs.idx]);
+            if (lane == 0) {
+                ptx::mbar_arrive(&tempty[rt.idx]);
+                ptx::mbar_arrive(&empty[rs.idx]);
+            }
+            if (et == 0) trace_chunk(p, 4, nch);
+            ++nch;
+            rt.next<NCS>();
             rs.next<NS>();
             if (gc + cg < sg.g1) return true;  // the segment continues in the next chunk
 
@@ -433,7 +471,7 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
         });
     }
 
-    if (threadIdx.x == 256) trace(p, 5);
+    if (threadIdx.x == C::kEpiThread0) trace(p, 5);
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) trace(p, 6);

@@ -11,10 +11,12 @@
 //              UMMA K-major SWIZZLE_128B image (consumed by tcgen05.mma in
 //              place, no conversion) | f32 scales[128] | 512 B pad (keeps every
 //              block 1024-B aligned for the SW128 atoms);
-//   sub4 block  8832 B: codes 8192 B = 128 rows x 64 B of nibbles, row r /
-//              16-code chunk c at r*64 + c*8, nibble order chosen so the
-//              converter's output words are byte-ordered (see pack_chunk4) |
-//              f32 scales[128] | u8 zero points[128].
+//   sub4 block  8832 B: codes 8192 B of nibbles stored column-chunk-major —
+//              the 32 codes [32q, 32q+32) of row r at q*2048 + r*16 (16-code
+//              halves at +0 / +8, nibble order per pack_chunk4) so the
+//              converter's per-row 16-byte loads are bank-conflict free and its
+//              output words come out in K order | f32 scales[128] | u8 zero
+//              points[128].
 // Rows past the end of a ragged tile are zero.
 #pragma once
 #include <cstdint>
@@ -27,6 +29,11 @@ constexpr int kCodes8Bytes = 16384; // 128 x 128 int8
 constexpr int kCodes4Bytes = 8192;  // 128 x 128 nibbles
 constexpr int kBlock8Bytes = 17408; // codes | scales | pad
 constexpr int kBlock4Bytes = 8832;  // codes | scales | zero points
+
+// byte offset of the 16-code chunk c (0..7) of row r inside a sub4 block
+__host__ __device__ inline uint32_t sub4_chunk_offset(uint32_t r, uint32_t c) {
+    return (c >> 1) * 2048u + r * 16u + (c & 1u) * 8u;
+}
 
 struct TileDesc {  // host-side bookkeeping of one tile
     int64_t codes_off;   // byte offset of the tile's group-0 block

@@ -16,12 +16,26 @@ torch.cuda.synchronize()
 t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
 t0.record(); dl.forward_codes(codes, scales, out=Y, opts=opts); t1.record(); torch.cuda.synchronize()
 print("event us", t0.elapsed_time(t1) * 1e3)
-buf = (C.c_ulonglong * (148 * 8))()
+buf = (C.c_ulonglong * (148 * 8 + 1024))()
 n = capi.lib().mq_debug_trace(buf)
-a = np.array(buf, dtype=np.float64).reshape(148, 8)
+raw = np.array(buf, dtype=np.float64)
+a = raw[:148*8].reshape(148, 8)
 base = a[:, 0][a[:, 0] > 0].min()
 a = np.where(a > 0, a - base, np.nan) / 1000.0
 names = ["start", "prod_pass1", "prod_after_gdw", "epi_first_tfull", "epi_seg_done", "epi_exit", "end"]
 for i, nm in enumerate(names):
     col = a[:, i]
     print(f"{nm:16s} min {np.nanmin(col):7.2f} med {np.nanmedian(col):7.2f} max {np.nanmax(col):7.2f} us")
+
+ch = raw[148*8:].reshape(16, 64)
+b = min(v for v in ch[:8].reshape(-1) if v > 0)
+print("CTA chunk timeline (kcycles): issue / full / mma_commit / conv_done / epi_done")
+for n in range(16):
+    row = ch[:5, n]
+    if row[1] == 0: continue
+    print(n, " ".join(f"{(v-b)/1000:7.2f}" if v > 0 else "    -  " for v in row))
+print("per group (kcycles): mma_after_waits / mma_after_commit / epi_after_tfull")
+for n in range(24):
+    row = ch[5:8, n]
+    if row[0] == 0: continue
+    print(n, " ".join(f"{(v-b)/1000:7.2f}" if v > 0 else "    -  " for v in row))
