@@ -116,6 +116,15 @@ mq_status mq_reassemble_output(const float* y8, int64_t n8, const float* y4, int
 int64_t mq_bench_inputs(int64_t m, int64_t n, int64_t k, double percent, uint64_t seed,
                         double* W, float* A, int32_t* promoted);
 
+/* Output-feature column-sharding plan (no reference counterpart —
+ * the reference is single-process). Host only, no device needed. Rank r of
+ * world W owns sub8 rows [r*n8/W, (r+1)*n8/W) and sub4 rows [r*n4/W, (r+1)*n4/W)
+ * and writes its outputs in gather order: local column j of rank r is
+ * original output column colmap[r*shard_cols + j] (sub8 rows first, then
+ * sub4; -1 marks padding up to shard_cols = max over ranks). colmap may be
+ * NULL (query shard_cols first); else it holds world*shard_cols entries. */
+mq_status mq_shard_plan(const mq_layer_desc* desc, int32_t world, int64_t* shard_cols, int32_t* colmap);
+
 /* fnv1a_hex (gemm.cpp:194-204) as a 64-bit value. */
 uint64_t mq_fnv1a(const void* data, uint64_t nbytes);
 

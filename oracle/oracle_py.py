@@ -65,6 +65,12 @@ def mqo():
         lib.mqo_reassemble.argtypes = [_P, _I64, _P, _I64, _P, _P, _I64, _I64, _P]
         lib.mqo_pack_nibbles.argtypes = [_P, _I64, _P]
         lib.mqo_unpack_nibbles.argtypes = [_P, _I64, _I64, _P]
+        for fn in ("mqo_quant_group_sym_f64", "mqo_quant_group_sym_f32"):
+            getattr(lib, fn).argtypes = [_P, _I64, C.c_int, C.c_int, _P, _P]
+        for fn in ("mqo_quant_group_asym_f64", "mqo_quant_group_asym_f32"):
+            getattr(lib, fn).argtypes = [_P, _I64, C.c_int, C.c_int, _P, _P, _P]
+        lib.mqo_rng_uniform_int.restype = _I64
+        lib.mqo_rng_uniform_int.argtypes = [_P, _I64, _I64]
         lib.mqo_rng_seed.argtypes = [_P, C.c_uint64]
         lib.mqo_rng_next.restype = C.c_uint64
         lib.mqo_rng_next.argtypes = [_P]
@@ -127,6 +133,45 @@ def normal_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
 
 
 # ------------------------------------------------------------- quantizers
+def quant_group_sym(x, bits: int, f16: bool = False):
+    """quantize_group_sym<double|float> (quant.hpp:117-140): (codes int8, scale f32)."""
+    x = np.ascontiguousarray(x)
+    codes = np.zeros(max(x.size, 1), np.int8)
+    sc = np.zeros(1, np.float32)
+    fn = mqo().mqo_quant_group_sym_f64 if x.dtype == np.float64 else mqo().mqo_quant_group_sym_f32
+    st = fn(_ptr(x), x.size, bits, int(f16), _ptr(codes), _ptr(sc))
+    if st:
+        raise OracleError(st, "group quantization")
+    return codes[: x.size], sc[0]
+
+
+def quant_group_asym(x, bits: int, f16: bool = False):
+    """quantize_group_asym<double|float> (quant.hpp:84-112): (codes u8, scale f32, zero point)."""
+    x = np.ascontiguousarray(x)
+    codes = np.zeros(max(x.size, 1), np.uint8)
+    sc = np.zeros(1, np.float32)
+    zp = np.zeros(1, np.uint8)
+    fn = mqo().mqo_quant_group_asym_f64 if x.dtype == np.float64 else mqo().mqo_quant_group_asym_f32
+    st = fn(_ptr(x), x.size, bits, int(f16), _ptr(codes), _ptr(sc), _ptr(zp))
+    if st:
+        raise OracleError(st, "group quantization")
+    return codes[: x.size], sc[0], int(zp[0])
+
+
+class Rng:
+    """Xoshiro256pp (rng.hpp:29-82) — the reference tests' generator."""
+
+    def __init__(self, seed: int):
+        self.st = (C.c_uint64 * 6)()
+        mqo().mqo_rng_seed(C.cast(self.st, _P), seed)
+
+    def normal(self) -> float:
+        return mqo().mqo_rng_normal(C.cast(self.st, _P))
+
+    def uniform_int(self, lo: int, hi: int) -> int:
+        return mqo().mqo_rng_uniform_int(C.cast(self.st, _P), lo, hi)
+
+
 @dataclass
 class QTensor:
     bits: int

@@ -27,6 +27,7 @@ from .mixquant import (  # noqa: F401
     reassemble_output,
     round_scale_f16,
     run_bench,
+    shard_plan,
     unpack_nibbles,
     validate_mixed_layer,
 )

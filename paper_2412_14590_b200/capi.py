@@ -72,6 +72,7 @@ PROTOTYPES = {
     "mq_reassemble_output": (C.c_int, [P, I64, P, I64, P, P, I64, I64, P]),
     "mq_bench_inputs": (I64, [I64, I64, I64, C.c_double, C.c_uint64, P, P, P]),
     "mq_fnv1a": (C.c_uint64, [P, C.c_uint64]),
+    "mq_shard_plan": (C.c_int, [C.POINTER(mq_layer_desc), I32, C.POINTER(I64), P]),
     "mq_layer_create": (C.c_int, [C.POINTER(mq_layer_desc), C.POINTER(mq_layer_opts), C.c_int, C.POINTER(P)]),
     "mq_layer_destroy": (None, [P]),
     "mq_layer_get_info": (C.c_int, [P, C.POINTER(mq_layer_info)]),

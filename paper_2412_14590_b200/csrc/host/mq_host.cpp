@@ -415,6 +415,27 @@ int64_t mq_bench_inputs(int64_t m, int64_t n, int64_t k, double percent, uint64_
     return np;
 }
 
+mq_status mq_shard_plan(const mq_layer_desc* d, int32_t world, int64_t* shard_cols, int32_t* colmap) {
+    if (!d || !shard_cols) return fail(MQ_USAGE, "mq_shard_plan: null argument");
+    if (world < 1) return fail(MQ_USAGE, "world must be >= 1");
+    if (d->n8 < 0 || d->n4 < 0 || d->n8 + d->n4 != d->out_features)
+        return fail(MQ_DATA, "index maps do not cover the output features");
+    auto lo = [&](int64_t n, int64_t r) { return n * r / world; };
+    int64_t sc = 0;
+    for (int64_t r = 0; r < world; ++r)
+        sc = std::max(sc, (lo(d->n8, r + 1) - lo(d->n8, r)) + (lo(d->n4, r + 1) - lo(d->n4, r)));
+    *shard_cols = sc;
+    if (!colmap) return MQ_OK;
+    for (int64_t r = 0; r < world; ++r) {
+        int64_t j = 0;
+        int32_t* row = colmap + r * sc;
+        for (int64_t i = lo(d->n8, r); i < lo(d->n8, r + 1); ++i) row[j++] = d->index_map8[i];
+        for (int64_t i = lo(d->n4, r); i < lo(d->n4, r + 1); ++i) row[j++] = d->index_map4[i];
+        for (; j < sc; ++j) row[j] = -1;
+    }
+    return MQ_OK;
+}
+
 uint64_t mq_fnv1a(const void* data, uint64_t n) {
     const auto* b = static_cast<const uint8_t*>(data);
     uint64_t h = 0xCBF29CE484222325ULL;

@@ -280,16 +280,12 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     L->tiles8 = (L->n8 + kTileRows - 1) / kTileRows;
     L->tiles4 = (L->n4 + kTileRows - 1) / kTileRows;
     if (o.world > 1) {
-        int64_t sc = 0;
-        for (int r = 0; r < o.world; ++r)
-            sc = std::max(sc, (lo(d->n8, r + 1) - lo(d->n8, r)) + (lo(d->n4, r + 1) - lo(d->n4, r)));
-        L->shard_cols = sc;
-        L->shard_colmap.assign(size_t(o.world * sc), -1);
-        for (int r = 0; r < o.world; ++r) {
-            int64_t j = 0;
-            for (int64_t i = lo(d->n8, r); i < lo(d->n8, r + 1); ++i) L->shard_colmap[r * sc + j++] = d->index_map8[i];
-            for (int64_t i = lo(d->n4, r); i < lo(d->n4, r + 1); ++i) L->shard_colmap[r * sc + j++] = d->index_map4[i];
+        if (mq_status st = mq_shard_plan(d, o.world, &L->shard_cols, nullptr)) {
+            delete L;
+            return st;
         }
+        L->shard_colmap.assign(size_t(o.world * L->shard_cols), -1);
+        mq_shard_plan(d, o.world, &L->shard_cols, L->shard_colmap.data());
     } else {
         L->shard_cols = L->N;
     }

@@ -210,6 +210,18 @@ def reassemble_output(y8, y4, map8, map4, out_features: int) -> np.ndarray:
     return out
 
 
+def shard_plan(layer: MixedLinearLayer, world: int):
+    """Output-feature column-sharding plan, host only: returns
+    (shard_cols, colmap [world, shard_cols]) — rank r's local column j is
+    original column colmap[r, j] (-1 = padding)."""
+    d = layer.desc()
+    sc = C.c_int64()
+    check(lib().mq_shard_plan(C.byref(d), world, C.byref(sc), None))
+    out = np.zeros(world * sc.value, np.int32)
+    check(lib().mq_shard_plan(C.byref(d), world, C.byref(sc), _p(out)))
+    return sc.value, out.reshape(world, sc.value)
+
+
 def bench_inputs(m: int, n: int, k: int, percent: float, seed: int = 1):
     """run_bench's synthetic inputs (gemm.cpp:211-227), byte-for-byte."""
     W = np.empty((n, k), np.float64)
