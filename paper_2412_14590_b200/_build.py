@@ -16,6 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libmixllm_b200.so")
+TEST_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "test_dropin")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
@@ -70,6 +71,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs,
               "-L" + os.path.join(CUDA, "lib64"), "-lcudart_static", "-ldl", "-lrt", "-lpthread"])
+    # the C++ drop-in test driver (reference call shapes over include/mixllm/mixquant.hpp)
+    tsrc = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    if os.path.exists(tsrc):
+        os.makedirs(os.path.dirname(TEST_BIN), exist_ok=True)
+        if force or _stale(TEST_BIN, [tsrc, LIB, os.path.join(ROOT, "include", "mixllm", "mixquant.hpp")]):
+            _run(["g++", "-std=gnu++20", "-O2", "-Wall", *INC, tsrc, "-o", TEST_BIN, "-L" + PKG, "-lmixllm_b200",
+                  "-Wl,-rpath," + PKG, "-L" + os.path.join(CUDA, "lib64"), "-lcudart_static", "-ldl", "-lrt",
+                  "-lpthread"])
     return LIB
 
 

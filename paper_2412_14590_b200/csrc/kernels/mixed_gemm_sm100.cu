@@ -335,7 +335,7 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
             rs.next<NS>();
             return true;
         });
-    } else {
+    } else if (int(threadIdx.x) >= C::kEpiThread0) {
         // ============================== epilogue ==============================
         const int et = threadIdx.x - C::kEpiThread0;  // 0 .. 128*NE-1
         const int e = et >> 7;                        // epilogue warpgroup

@@ -16,7 +16,7 @@ def _built() -> None:
     """Build the product library and the oracle in-tree if they are missing."""
     from paper_2412_14590_b200 import _build
 
-    if not os.path.exists(_build.LIB):
+    if not os.path.exists(_build.LIB) or not os.path.exists(_build.TEST_BIN):
         _build.build()
     import oracle_py
 

@@ -209,3 +209,15 @@ def test_run_bench_checksum(cuda, golden):
     c = golden["cases"][0]
     r = mq.run_bench(c["m"], c["n"], c["k"], c["percent"], repeats=2)
     assert r["checksum"] == c["out_f32"]
+
+
+def test_cpp_dropin_binary(cuda):
+    """The reference's C++ call shapes (run_bench, execute_mixed_linear,
+    execute_mixed_on_codes, a quantized_forward-style chain) compiled against
+    include/mixllm/mixquant.hpp: golden checksums, errors before compute."""
+    import os
+    import subprocess
+    from paper_2412_14590_b200 import _build
+    assert os.path.exists(_build.TEST_BIN), "tests/cpp/_bin/test_dropin not built (run __graft_entry__.build())"
+    r = subprocess.run([_build.TEST_BIN, "--gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
