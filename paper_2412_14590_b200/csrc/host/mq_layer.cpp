@@ -97,14 +97,22 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
         return fail(MQ_USAGE, "token_tile must be 16, 32, 64 or 128");
     pl->tb = static_cast<int>((M + pl->bn - 1) / pl->bn);
     pl->split = o->mode == MQ_FAST && o->ksplit != 1;
-    pl->mode = o->mode == MQ_EXACT ? kExactGroup : (pl->per_token ? kFastToken : kFastGroup);
+    pl->mode = o->mode == MQ_EXACT ? (pl->per_token ? kExactToken : kExactGroup) : (pl->per_token ? kFastToken : kFastGroup);
     pl->pdl = o->no_pdl == 0;
     return MQ_OK;
 }
 
+// Every CTA must own at least one group: an empty range inside an item would
+// never arrive on the item's stream-K counter (the reduction counts the CTAs
+// ca..cz that overlap it). P <= X, so strictly increasing cuts always exist.
 void fill_cuts(GemmParams* p) {
     const Schedule S(*p);
+    const int32_t X = static_cast<int32_t>(S.X);
     for (int c = 0; c <= p->P; ++c) p->cuts[c] = static_cast<int32_t>(S.cut(c));
+    for (int c = 1; c < p->P; ++c) p->cuts[c] = std::max(p->cuts[c], p->cuts[c - 1] + 1);
+    for (int c = p->P - 1; c >= 1; --c) p->cuts[c] = std::min(p->cuts[c], p->cuts[c + 1] - 1);
+    p->cuts[0] = 0;
+    p->cuts[p->P] = X;
 }
 
 // The launch grid and the stream-K cost weights (bytes streamed per group,

@@ -306,8 +306,11 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
         Ring rs, ra;
         int nch = 0;
         for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
+            // wait on EVERY chunk's full barrier, sub8 ones included: a role that
+            // skipped chunks could run two phases ahead of a stage's barrier and
+            // read the parity of an older phase as "complete" (stale stage data)
+            ptx::mbar_wait(&full[rs.idx], rs.ph);
             if (!ti.is8) {
-                ptx::mbar_wait(&full[rs.idx], rs.ph);
                 ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
                 const uint8_t* st = stage(rs.idx);
                 for (int j = wg; j < cg; j += NC) {
@@ -349,11 +352,17 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
         Ring rs, rt;
         bool first_group = true;
         float acc[BNE];
+        float sat[MODE == kExactToken ? BNE : 1];  // per-token s_a of this warpgroup's tokens
         int nch = 0;
         for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
             if (gc == sg.g0) {
 #pragma unroll
                 for (int j = 0; j < BNE; ++j) acc[j] = 0.0f;
+                if constexpr (MODE == kExactToken) {
+                    const int64_t mb = int64_t(sg.tb) * BN + c0;
+#pragma unroll
+                    for (int j = 0; j < BNE; ++j) sat[j] = mb + j < p.M ? __ldg(p.sa + mb + j) : 0.0f;
+                }
             }
             ptx::mbar_wait(&full[rs.idx], rs.ph);
             ptx::mbar_wait(&tfull[rt.idx], rt.ph);
@@ -389,6 +398,8 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                             if constexpr (MODE == kExactGroup) {
                                 // gemm.cpp:81 — out += gs * (s_a * s_w), no contraction
                                 acc[jj] = __fadd_rn(acc[jj], __fmul_rn(gs, __fmul_rn(sav[jj], sw)));
+                            } else if constexpr (MODE == kExactToken) {
+                                acc[jj] = __fadd_rn(acc[jj], __fmul_rn(gs, __fmul_rn(sat[jj], sw)));
                             } else if constexpr (MODE == kFastGroup) {
                                 acc[jj] = __fmaf_rn(gs, __fmul_rn(sav[jj], sw), acc[jj]);
                             } else {
@@ -514,6 +525,7 @@ cudaError_t launch_bn(const GemmParams& p, const void* tmap, const void* tmap_sa
         case kExactGroup: return launch_bn_mode<BN, kExactGroup>(p, tmap, tmap_sa, pdl, s);
         case kFastGroup: return launch_bn_mode<BN, kFastGroup>(p, tmap, tmap_sa, pdl, s);
         case kFastToken: return launch_bn_mode<BN, kFastToken>(p, tmap, tmap_sa, pdl, s);
+        case kExactToken: return launch_bn_mode<BN, kExactToken>(p, tmap, tmap_sa, pdl, s);
         default: return launch_bn_mode<BN, kDumpPartials>(p, tmap, tmap_sa, pdl, s);
     }
 }

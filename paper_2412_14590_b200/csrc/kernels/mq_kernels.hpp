@@ -12,7 +12,8 @@ enum GemmMode : int {
     kExactGroup = 0,  // reference op order (f32 mul then add), whole work items
     kFastGroup = 1,   // FFMA rescale, group-wise s_a, stream-K splits
     kFastToken = 2,   // per-token s_a factored out: acc += gs*s_w, y = s_a*acc
-    kDumpPartials = 3 // int32 group sums to a [G, M, rows] buffer
+    kDumpPartials = 3, // int32 group sums to a [G, M, rows] buffer
+    kExactToken = 4   // reference op order with a per-token s_a broadcast over groups
 };
 
 // Everything the kernel needs is scalar: tile descriptors and the stream-K

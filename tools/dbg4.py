@@ -10,7 +10,7 @@ dl = mq.DeviceLayer(L)
 dA = torch.from_numpy(A).cuda()
 codes, scales = mq.quantize_act(dA, 128)
 Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
-opts = mq.exec_opts(capi.MQ_FAST, 128, pdl=False)
+opts = mq.exec_opts(capi.MQ_FAST, 128, pdl=False, ksplit=int(os.environ.get("KSPLIT", "0")))
 for _ in range(3): dl.forward_codes(codes, scales, out=Y, opts=opts)
 torch.cuda.synchronize()
 t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
@@ -30,7 +30,7 @@ for i, nm in enumerate(names):
 ch = raw[148*8:].reshape(16, 64)
 b = min(v for v in ch[:8].reshape(-1) if v > 0)
 print("CTA chunk timeline (kcycles): issue / full / mma_commit / conv_done / epi_done")
-for n in range(16):
+for n in range(40):
     row = ch[:5, n]
     if row[1] == 0: continue
     print(n, " ".join(f"{(v-b)/1000:7.2f}" if v > 0 else "    -  " for v in row))

@@ -114,6 +114,25 @@ int main() {
             printf("ldg  total=%4dMB blocks=%d: %8.2f us  %7.0f GB/s\n", total_mb, blocks, us, tot / us / 1e3);
         }
     }
+    // per-CTA streaming cap: few CTAs, 2 MB each
+    for (int ctas : {1, 8, 32, 74, 113, 148}) {
+        for (int chunk : {16384, 32768}) {
+            const int depth = chunk == 16384 ? 12 : 6;
+            const size_t per = size_t(2) << 20;
+            const int smem = chunk * depth + 1024;
+            cudaFuncSetAttribute(bulk_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            bulk_ring<<<ctas, 128, smem>>>(buf, per, chunk, depth, 1, sink);
+            cudaEventRecord(e0);
+            for (int r = 0; r < 10; ++r) bulk_ring<<<ctas, 128, smem>>>(buf + (r % 2) * (400u << 20), per, chunk, depth, 1, sink);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double us = ms * 1e3 / 10;
+            printf("percta ctas=%3d chunk=%5d depth=%2d: %8.2f us  %7.1f GB/s per CTA  %7.0f GB/s total\n", ctas, chunk, depth, us,
+                   per / us / 1e3, per * ctas / us / 1e3);
+        }
+    }
     printf("err %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
     return 0;
 }
