@@ -2,11 +2,12 @@
 """bench.py — MixLLM W4/W8-A8 mixed-precision linear on B200.
 
 Workload (BASELINE.json configs[1]): the Llama-3.1-8B decoder-layer linear
-stack (q, k, v, o, gate, up, down), 10% of output features 8-bit, 4-bit
+stack (QKV / O / gate-up / down), 10% of output features 8-bit, 4-bit
 group-128 weights, int8 group-wise activations (the reference's semantics,
 proj/src/gemm.cpp:183-192), MQ_FAST mode, fp16 output, batch M (default 16).
-One STEP = the 7 projections' full dynamic path (activation quantization +
-mixed GEMM + scatter) = 14 kernel launches, replayed from a CUDA graph.
+One STEP = the decoder layer's 4 fused projections (qkv, o, gate_up, down), each
+the full dynamic path (activation quantization + mixed GEMM + scatter) = 8 kernel
+launches, replayed from a CUDA graph.
 Synthetic run_bench-generator weights/activations (no checkpoints). Two
 device replicas of the stack (2 x ~128 MB) alternate between steps so the
 weights stream from HBM, not L2 (126 MB).
@@ -35,8 +36,12 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 import numpy as np  # noqa: E402
 
-SHAPES_8B = [("q_proj", 4096, 4096), ("k_proj", 1024, 4096), ("v_proj", 1024, 4096), ("o_proj", 4096, 4096),
-             ("gate_proj", 14336, 4096), ("up_proj", 14336, 4096), ("down_proj", 4096, 14336)]
+# BASELINE configs[1]: "Llama-3.1-8B linear shapes (QKV/O/gate-up/down)". q/k/v share their
+# input and so do gate/up, so each pair/triple is one fused layer (output features
+# concatenated; every output feature is an independent dot product, so this is
+# arithmetically identical to separate q, k, v / gate, up layers): 4 layers per step.
+SHAPES_8B = [("qkv_proj", 4096 + 1024 + 1024, 4096), ("o_proj", 4096, 4096),
+             ("gate_up_proj", 2 * 14336, 4096), ("down_proj", 4096, 14336)]
 PERCENT = 0.10
 GROUP = 128
 METRIC = "mixed-precision linear TOPS & latency vs batch (1-512); % HBM / int8-TC peak"
@@ -310,7 +315,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int8 (int32 accum, f32 rescale, f16 out)",
             "data": "synthetic (run_bench generator weights, randn activations)",
-            "config": {"workload": f"llama3.1-8b decoder-layer linear stack q,k,v,o,gate,up,down; batch {M}; "
+            "config": {"workload": f"llama3.1-8b decoder-layer linear stack (fused qkv 6144x4096, o 4096x4096, fused gate_up 28672x4096, down 4096x14336); batch {M}; "
                                    f"{int(PERCENT * 100)}% 8-bit output features; W4 g128 asym + W8 sym; "
                                    f"A8 group-wise (reference semantics); mode {args.mode}; fp16 out",
                        "batch": M, "group": GROUP, "percent_8bit": PERCENT,
@@ -319,11 +324,11 @@ def run_ours(args):
                        "cuda_graph": world == 1},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                         "kernel": "mixed_gemm_tc_kernel (7 launches/step; bytes and time summed)",
+                         "kernel": f"mixed_gemm_tc_kernel ({len(SHAPES_8B)} launches/step; bytes and time summed)",
                          "peak_kind": peak_kind,
                          "k2_bytes_per_step": int(head["k2_bytes"]), "k2_ms_per_step": round(head["ms_k2"], 5)},
             "int8_peak_tops_measured": round(int8_peak, 1) if int8_peak else None,
-            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps * 14, "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps * 2 * len(SHAPES_8B), "clocks": clocks,
             "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
@@ -334,7 +339,7 @@ def run_ours(args):
 # ----------------------------------------------------------- reference
 def cpu_reference(M, budget_s=12.0, steps=None, warmup=0):
     """The reference's own implementation (oracle/_ref) on this host's cores:
-    one step = execute_mixed_linear for the 7 projections (workers = nproc)."""
+    one step = execute_mixed_linear for the 4 fused projections (workers = nproc)."""
     import oracle_py as O
 
     cores = os.cpu_count() or 1
@@ -369,7 +374,7 @@ def cpu_reference(M, budget_s=12.0, steps=None, warmup=0):
     ms = sum(times) / len(times)
     return {"value": round(ops / (ms * 1e-3) / 1e12, 6), "unit": "TOPS", "cores": cores, "kind": kind,
             "ms_per_step": round(ms, 2),
-            "sample": f"{len(times)} step(s) of the full 7-projection stack at batch {M} "
+            "sample": f"{len(times)} step(s) of the full 4-layer (qkv, o, gate_up, down) stack at batch {M} "
                       f"(reference execute_mixed_linear, workers={cores}, fast I2F)"}
 
 
@@ -384,7 +389,7 @@ def run_reference(args):
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": budget_steps, "warmup": min(args.warmup, 1),
             "ms_per_step": res.get("ms_per_step"), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int8 (int32 accum, f32 rescale, f32 out)", "data": "synthetic",
-            "config": {"workload": f"llama3.1-8b decoder-layer linear stack q,k,v,o,gate,up,down; batch {args.batch}; "
+            "config": {"workload": f"llama3.1-8b decoder-layer linear stack (fused qkv 6144x4096, o 4096x4096, fused gate_up 28672x4096, down 4096x14336); batch {args.batch}; "
                                    f"{int(PERCENT * 100)}% 8-bit output features; W4 g128 asym + W8 sym; "
                                    f"A8 group-wise (reference semantics); reference CPU path",
                        "batch": args.batch},

@@ -49,30 +49,36 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError(f"build failed: {cmd[0]} {cmd[-1]}")
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: tuple = (), lib: str | None = None,
+          obj: str | None = None) -> str:
+    """defines/lib/obj: development variants (e.g. -DMQ_NS_MAX=12) built beside the product library."""
+    lib_path = lib or LIB
+    obj_dir = obj or OBJ
+    os.makedirs(obj_dir, exist_ok=True)
     deps = _deps()
     objs = []
     for src in CU_SRCS:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, os.path.basename(src) + ".o")
+        o = os.path.join(obj_dir, os.path.basename(src) + ".o")
         objs.append(o)
         if force or _stale(o, [s] + deps):
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *defines,
                   "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
                   *INC, "-c", s, "-o", o])
     for src in CPP_SRCS:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, os.path.basename(src) + ".o")
+        o = os.path.join(obj_dir, os.path.basename(src) + ".o")
         objs.append(o)
         if force or _stale(o, [s] + deps):
-            _run(["g++", "-std=gnu++20", "-O2", "-ffp-contract=off", "-fPIC", "-Wall", "-Wno-unused-function",
+            _run(["g++", *defines, "-std=gnu++20", "-O2", "-ffp-contract=off", "-fPIC", "-Wall", "-Wno-unused-function",
                   *INC, "-c", s, "-o", o])
-    if force or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs,
+    if force or _stale(lib_path, objs):
+        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib_path, *objs,
               "-L" + os.path.join(CUDA, "lib64"), "-lcudart_static", "-ldl", "-lrt", "-lpthread"])
     # the C++ drop-in test driver (reference call shapes over include/mixllm/mixquant.hpp)
     tsrc = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    if lib is not None:
+        return lib_path
     if os.path.exists(tsrc):
         os.makedirs(os.path.dirname(TEST_BIN), exist_ok=True)
         if force or _stale(TEST_BIN, [tsrc, LIB, os.path.join(ROOT, "include", "mixllm", "mixquant.hpp")]):

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmixllm_b200.so")
+LIB_PATH = os.environ.get("MQ_LIB") or os.path.join(_HERE, "libmixllm_b200.so")  # MQ_LIB: development variants
 
 P = C.c_void_p
 I64 = C.c_int64

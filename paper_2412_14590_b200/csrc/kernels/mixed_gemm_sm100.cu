@@ -53,15 +53,26 @@ struct TcCfg {
     static constexpr int kOffB = kRaw;                     // [GPS][BN][128] int8, SW128
     static constexpr int kOffSa = kOffB + GPS * BN * 128;  // [GPS][BN] f32
     static constexpr int kStageBytes = ((kOffSa + GPS * BN * 4) + 1023) / 1024 * 1024;
-    static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/;
-    static constexpr int NS0 = (kSmemMax - kFixed) / kStageBytes;
-    static constexpr int NS = NS0 > 8 ? 8 : NS0;
-    static constexpr int NCS = 2;                            // chunk slots of the TMEM rings
-    static constexpr uint32_t kAccCols = NCS * GPS * BN;     // int32 accumulators
-    static constexpr uint32_t kACol0 = kAccCols;             // A ring: NCS*GPS tiles x 32 cols
-    static constexpr uint32_t kTmemNeed = kAccCols + NCS * GPS * 32;
+    // TMEM rings (512 columns): NT accumulator chunk slots of GPS x BN int32
+    // columns, NA A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
+    static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
+    static constexpr int NT = BN >= 128 ? 3 : 2;
+    static constexpr int NA = int((512u - NT * kAccPerChunk) / kAPerChunk) > 4 ? 4 : int((512u - NT * kAccPerChunk) / kAPerChunk);
+    static constexpr uint32_t kAccCols = NT * kAccPerChunk;
+    static constexpr uint32_t kACol0 = kAccCols;
+    static constexpr uint32_t kTmemNeed = kAccCols + NA * kAPerChunk;
     static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
-    static_assert(kTmemNeed <= 512, "TMEM budget");
+    static_assert(kTmemNeed <= 512 && NA >= 2, "TMEM budget");
+    // meta ring (per accumulator slot): weight scales [GPS][128] + act scales [GPS][BN],
+    // copied out of the stage by the converter so stages free up before the epilogue runs
+    static constexpr int kMetaSlot = GPS * (128 + BN) * 4;
+    static constexpr int kMetaBytes = NT * kMetaSlot;
+    static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/ + kMetaBytes;
+    static constexpr int NS0 = (kSmemMax - kFixed) / kStageBytes;
+#ifndef MQ_NS_MAX
+#define MQ_NS_MAX 8
+#endif
+    static constexpr int NS = NS0 > MQ_NS_MAX ? MQ_NS_MAX : NS0;
     static constexpr int NE = BN <= 64 ? 1 : 2;  // epilogue warpgroups
     static constexpr int NC = BN <= 32 ? 2 : 1;  // converter warpgroups (decode is conversion-bound)
     static constexpr int BNE = BN / NE;          // tokens per epilogue warpgroup
@@ -69,6 +80,7 @@ struct TcCfg {
     static constexpr int kThreads = 128 * (1 + NC + NE);
     static constexpr int kSmem = kFixed + NS * kStageBytes;
     static_assert(NS >= 2, "pipeline needs at least two stages");
+    static_assert(GPS * BN <= 128, "act-scale copy: one converter thread per value");
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -144,21 +156,23 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1)
 mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_constant__ CUtensorMap tmap_sa,
                      const __grid_constant__ GemmParams p) {
     using C = TcCfg<BN>;
-    constexpr int NS = C::NS, NE = C::NE, BNE = C::BNE, GPS = C::GPS, NCS = C::NCS, NC = C::NC;
+    constexpr int NS = C::NS, NE = C::NE, BNE = C::BNE, GPS = C::GPS, NA = C::NA, NT = C::NT, NC = C::NC;
     constexpr bool kSa = (MODE == kExactGroup || MODE == kFastGroup);
     extern __shared__ uint8_t smem_raw[];
     // 1024-B aligned base (SWIZZLE_128B atoms), derived from smem_raw so the
     // compiler keeps shared-space provenance (LDS/STS, not generic LD/ST)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stages = smem;  // [NS][kStageBytes]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * C::kStageBytes);
+    float* meta = reinterpret_cast<float*>(stages + NS * C::kStageBytes);  // [NT] x (sw [GPS][128] | sa [GPS][BN])
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * C::kStageBytes + C::kMetaBytes);
     uint64_t* full = bars;                 // [NS] producer (expect_tx)
-    uint64_t* empty = full + NS;           // [NS] MMA commit + epilogue warps
-    uint64_t* afull = empty + NS;          // [NCS] converter -> MMA (TMEM A tiles written)
-    uint64_t* aempty = afull + NCS;        // [NCS] MMA commit -> converter
-    uint64_t* tfull = aempty + NCS;        // [NCS] MMA commit -> epilogue
-    uint64_t* tempty = tfull + NCS;        // [NCS] epilogue -> MMA
-    uint64_t* tmem_ready = tempty + NCS;   // warp 1 -> everyone using TMEM
+    uint64_t* empty = full + NS;           // [NS] MMA commit + converter warps
+    uint64_t* afull = empty + NS;          // [NA] converter -> MMA (TMEM A tiles + meta written)
+    uint64_t* aempty = afull + NA;         // [NA] MMA commit -> converter
+    uint64_t* tfull = aempty + NA;         // [NT] MMA commit -> epilogue
+    uint64_t* tempty = tfull + NT;         // [NT] epilogue -> MMA / converter (acc + meta slot free)
+    uint64_t* mfull = tempty + NT;         // [NT] converter -> epilogue (meta slot written)
+    uint64_t* tmem_ready = mfull + NT;     // warp 1 -> everyone using TMEM
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_ready + 1);
     int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
@@ -168,13 +182,16 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1 + 4 * NE);
+            ptx::mbar_init(&empty[s], 1 + 4 * NC);
         }
-        for (int i = 0; i < NCS; ++i) {
+        for (int i = 0; i < NA; ++i) {
             ptx::mbar_init(&afull[i], 4 * NC);
             ptx::mbar_init(&aempty[i], 1);
+        }
+        for (int i = 0; i < NT; ++i) {
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 4 * NE);
+            ptx::mbar_init(&mfull[i], 4 * NC);
         }
         ptx::mbar_init(tmem_ready, 1);
         ptx::fence_barrier_init();
@@ -260,7 +277,7 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
         int nch = 0;
         for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
             ptx::mbar_wait(&full[rs.idx], rs.ph);
-            if (!ti.is8) ptx::mbar_wait(&afull[ra.idx], ra.ph);
+            ptx::mbar_wait(&afull[ra.idx], ra.ph);
             ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
             ptx::tc_fence_after();
             if (lane == 0) trace_chunk(p, 1, nch);
@@ -286,13 +303,13 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                     }
                 }
                 ptx::tc_commit(&tfull[rt.idx]);
-                if (!ti.is8) ptx::tc_commit(&aempty[ra.idx]);
+                ptx::tc_commit(&aempty[ra.idx]);
                 ptx::tc_commit(&empty[rs.idx]);
             }
             __syncwarp();
             if (lane == 0) trace_chunk(p, 2, nch++);
-            if (!ti.is8) ra.next<NCS>();
-            rt.next<NCS>();
+            ra.next<NA>();
+            rt.next<NT>();
             rs.next<NS>();
             return true;
         });
@@ -303,17 +320,22 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
         ptx::mbar_wait(tmem_ready, 0);
         ptx::tc_fence_after();
         const uint32_t tmem_row = *reinterpret_cast<volatile uint32_t*>(tmem_holder) + (uint32_t((warp & 3) * 32) << 16);
-        Ring rs, ra;
+        Ring rs, ra, rt;
         int nch = 0;
         for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
-            // wait on EVERY chunk's full barrier, sub8 ones included: a role that
-            // skipped chunks could run two phases ahead of a stage's barrier and
-            // read the parity of an older phase as "complete" (stale stage data)
+            // every chunk (sub8 too): wait for the stage, a free A slot and a free
+            // meta slot, then (sub4) convert codes into TMEM and (all) copy the
+            // chunk's weight / activation scales into the meta ring, so the stage
+            // is released by the converter + MMA, never by the epilogue.
             ptx::mbar_wait(&full[rs.idx], rs.ph);
-            if (!ti.is8) {
-                ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
-                const uint8_t* st = stage(rs.idx);
-                for (int j = wg; j < cg; j += NC) {
+            if (threadIdx.x == 128) trace_chunk(p, 5, nch);
+            ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
+            ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
+            if (threadIdx.x == 128) trace_chunk(p, 6, nch);
+            const uint8_t* st = stage(rs.idx);
+            float* msw = meta + rt.idx * (C::kMetaSlot / 4);
+            for (int j = wg; j < cg; j += NC) {
+                if (!ti.is8) {
                     const uint8_t* raw = st + j * kBlock4Bytes;
                     const uint32_t kk = uint32_t(128 - raw[kCodes4Bytes + 512 + r]) * 0x01010101u;
                     uint32_t v[32];
@@ -326,15 +348,25 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                         unpack_word(w.w, kk, v[q * 8 + 6], v[q * 8 + 7]);
                     }
                     if (!(p.dbg & 2)) ptx::tmem_st32(tmem_row + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32), v);
+                    msw[j * 128 + r] = reinterpret_cast<const float*>(raw + kCodes4Bytes)[r];
+                } else {
+                    msw[j * 128 + r] = reinterpret_cast<const float*>(st + j * kBlock8Bytes + kCodes8Bytes)[r];
                 }
-                ptx::tmem_wait_st();
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&afull[ra.idx]);
-                ra.next<NCS>();
+            }
+            if (kSa && wg == 0 && r < cg * BN)
+                msw[GPS * 128 + r] = reinterpret_cast<const float*>(st + C::kOffSa)[r];
+            if (!ti.is8) ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                ptx::mbar_arrive(&mfull[rt.idx]);
+                ptx::mbar_arrive(&afull[ra.idx]);
+                ptx::mbar_arrive(&empty[rs.idx]);
             }
             if (threadIdx.x == 128) trace_chunk(p, 3, nch);
             ++nch;
+            ra.next<NA>();
+            rt.next<NT>();
             rs.next<NS>();
             return true;
         });
@@ -349,7 +381,7 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
         ptx::tc_fence_after();
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
         griddep_wait();  // workspace / scales / output of this launch are ours now
-        Ring rs, rt;
+        Ring rt;
         bool first_group = true;
         float acc[BNE];
         float sat[MODE == kExactToken ? BNE : 1];  // per-token s_a of this warpgroup's tokens
@@ -364,16 +396,16 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                     for (int j = 0; j < BNE; ++j) sat[j] = mb + j < p.M ? __ldg(p.sa + mb + j) : 0.0f;
                 }
             }
-            ptx::mbar_wait(&full[rs.idx], rs.ph);
+            ptx::mbar_wait(&mfull[rt.idx], rt.ph);
             ptx::mbar_wait(&tfull[rt.idx], rt.ph);
             ptx::tc_fence_after();
             if (first_group && et == 0) trace(p, 3);
             first_group = false;
-            const uint8_t* st = stage(rs.idx);
+            const float* msw = meta + rt.idx * (C::kMetaSlot / 4);
             const int64_t m0 = int64_t(sg.tb) * BN + c0;  // first token of this warpgroup
             for (int j = 0; j < cg; ++j) {
-                const float sw = reinterpret_cast<const float*>(st + j * ti.blk + (ti.is8 ? kCodes8Bytes : kCodes4Bytes))[r];
-                const float* sav = reinterpret_cast<const float*>(st + C::kOffSa) + j * BN + c0;
+                const float sw = msw[j * 128 + r];
+                const float* sav = msw + GPS * 128 + j * BN + c0;
                 const uint32_t tcol = uint32_t((rt.idx * GPS + j) * BN + c0);
 #pragma unroll
                 for (int ch = 0; ch < BNE / 16; ++ch) {
@@ -411,14 +443,10 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                ptx::mbar_arrive(&tempty[rt.idx]);
-                ptx::mbar_arrive(&empty[rs.idx]);
-            }
+            if (lane == 0) ptx::mbar_arrive(&tempty[rt.idx]);
             if (et == 0) trace_chunk(p, 4, nch);
             ++nch;
-            rt.next<NCS>();
-            rs.next<NS>();
+            rt.next<NT>();
             if (gc + cg < sg.g1) return true;  // the segment continues in the next chunk
 
             // ---------------- end of segment: output or stream-K partial

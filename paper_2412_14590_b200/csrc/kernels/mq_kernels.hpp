@@ -59,7 +59,10 @@ struct GemmParams {
 cudaError_t launch_mixed_gemm_tc(const GemmParams& p, const void* tmap_act, const void* tmap_sa, int token_tile,
                                  int mode, bool pdl, cudaStream_t stream);
 // groups of a sub4 tile per pipeline stage (sub8: half) for a token tile
-constexpr int gemm_gps(int token_tile) { return token_tile <= 32 ? 4 : (token_tile == 64 ? 2 : 1); }
+#ifndef MQ_GPS_SMALL
+#define MQ_GPS_SMALL 4
+#endif
+constexpr int gemm_gps(int token_tile) { return token_tile <= 32 ? MQ_GPS_SMALL : (token_tile == 64 ? 2 : 1); }
 int gemm_stages(int token_tile);
 // SIMT debug kernel (same layout, exact op order); parity aid, not the product.
 cudaError_t launch_mixed_gemm_simt(const GemmParams& p, const int8_t* codes, int64_t ldc,

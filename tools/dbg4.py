@@ -29,13 +29,8 @@ for i, nm in enumerate(names):
 
 ch = raw[148*8:].reshape(16, 64)
 b = min(v for v in ch[:8].reshape(-1) if v > 0)
-print("CTA chunk timeline (kcycles): issue / full / mma_commit / conv_done / epi_done")
+print("CTA chunk timeline (kcycles): issue / mma_start / mma_commit / conv_done / epi_done / conv_full / conv_waits")
 for n in range(40):
-    row = ch[:5, n]
+    row = ch[:7, n]
     if row[1] == 0: continue
-    print(n, " ".join(f"{(v-b)/1000:7.2f}" if v > 0 else "    -  " for v in row))
-print("per group (kcycles): mma_after_waits / mma_after_commit / epi_after_tfull")
-for n in range(24):
-    row = ch[5:8, n]
-    if row[0] == 0: continue
     print(n, " ".join(f"{(v-b)/1000:7.2f}" if v > 0 else "    -  " for v in row))
