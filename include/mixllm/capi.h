@@ -232,6 +232,16 @@ mq_status mq_mixed_linear(mq_layer_t layer, const void* A, mq_dtype a_dtype, int
                           void* workspace, int32_t* err, void* stream);
 size_t mq_mixed_linear_workspace_bytes(mq_layer_t layer, int64_t M, const mq_exec_opts* opts);
 
+/* Split form of mq_mixed_linear for callers that feed ONE quantized activation
+ * to several layers with the same K, M and options (e.g. separate q/k/v or
+ * gate/up layers): mq_quantize_act_ws runs K1 into the engine activation layout
+ * (EAL) inside `workspace` (>= mq_mixed_linear_workspace_bytes); then any number
+ * of mq_mixed_linear_ws calls run K2 on it. Same results as mq_mixed_linear. */
+mq_status mq_quantize_act_ws(mq_layer_t layer, const void* A, mq_dtype a_dtype, int64_t M,
+                             const mq_exec_opts* opts, void* workspace, int32_t* err, void* stream);
+mq_status mq_mixed_linear_ws(mq_layer_t layer, int64_t M, const void* workspace, void* Y,
+                             mq_dtype out_dtype, const mq_exec_opts* opts, void* stream);
+
 /* Debug / parity: the int32 group partial sums S[g, m, r] = sum_i a*(w - z)
  * (the step-1 integer accumulator, gemm.cpp:64-75) of one sub-problem,
  * computed by the same tcgen05 pipeline. which: 0 = sub8, 1 = sub4.

@@ -83,6 +83,8 @@ PROTOTYPES = {
     "mq_mixed_linear": (C.c_int, [P, P, C.c_int, I64, P, C.c_int, C.POINTER(mq_exec_opts), P, P, P]),
     "mq_mixed_linear_workspace_bytes": (C.c_size_t, [P, I64, C.POINTER(mq_exec_opts)]),
     "mq_gemm_partials": (C.c_int, [P, P, I64, I64, I32, P, P]),
+    "mq_quantize_act_ws": (C.c_int, [P, P, C.c_int, I64, C.POINTER(mq_exec_opts), P, P, P]),
+    "mq_mixed_linear_ws": (C.c_int, [P, I64, P, P, C.c_int, C.POINTER(mq_exec_opts), P]),
     "mq_permute_gathered": (C.c_int, [P, P, I32, I64, I64, I64, P, C.c_int, P]),
 }
 

@@ -7,7 +7,6 @@
 // packing happens once in mq_layer_create and forwards only stream weights.
 #include <cuda.h>
 #include <cuda_runtime.h>
-#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <climits>
@@ -57,18 +56,6 @@ mq_status cuda_fail(cudaError_t e, const char* what) {
         if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
     } while (0)
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            p = nullptr;
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }();
-    return fn;
-}
-
 int auto_token_tile(int64_t M) {
     if (M <= 16) return 16;
     if (M <= 32) return 32;
@@ -77,9 +64,33 @@ int auto_token_tile(int64_t M) {
 }
 
 struct Plan {
-    int bn, tb, mode, per_token;
-    bool split, pdl;
+    int bn, tb, mode, per_token, C, units;
+    int64_t Mpad;
+    bool pdl, rotate;
 };
+
+// Cluster size of the paired split-K schedule (mq_kernels.hpp): the largest
+// even C <= 8 whose grid still fits in one wave of co-resident clusters; at
+// decode sizes the K-slices keep every SM streaming. Exact mode keeps the
+// reference's ascending group order per output, so it never splits.
+int choose_cluster(const mq_layer_s* L, const Plan& pl, int ksplit) {
+    if (pl.mode == kExactGroup || pl.mode == kExactToken || ksplit == 1) return 1;
+    if (ksplit >= 2) return std::min(8, ksplit & ~1);
+    const int64_t U1 = L->tiles8 + (L->tiles4 + 1) / 2;
+    if (pl.tb > 1) return 1;  // token-tiled (prefill) launches are tensor-bound: one tile per CTA
+    static thread_local int cache[4][2][9] = {};  // [bn][token mode][C] -> co-resident clusters (+1)
+    const int bi = pl.bn == 16 ? 0 : pl.bn == 32 ? 1 : pl.bn == 64 ? 2 : 3, ti = pl.mode == kFastToken;
+    int best = 2;
+    for (int C = 8; C >= 2; C -= 2) {
+        int& n = cache[bi][ti][C];
+        if (n == 0) n = 1 + gemm_max_clusters(pl.bn, pl.mode, C);
+        if (n > 1 && U1 * pl.tb <= int64_t(n - 1)) {
+            best = C;
+            break;
+        }
+    }
+    return best;
+}
 
 mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
     mq_exec_opts d{};
@@ -92,83 +103,34 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
                                   std::to_string(act_group) + ", weight group " + std::to_string(L->group) +
                                   "); per-token activations use act_group = K");
     if (o->mode != MQ_EXACT && o->mode != MQ_FAST) return fail(MQ_USAGE, "unknown mode");
+    if (o->ksplit < 0 || o->ksplit > 8) return fail(MQ_USAGE, "ksplit must be 0 (auto), 1 (none) or a cluster size <= 8");
     pl->bn = o->token_tile ? o->token_tile : auto_token_tile(M);
     if (pl->bn != 16 && pl->bn != 32 && pl->bn != 64 && pl->bn != 128)
         return fail(MQ_USAGE, "token_tile must be 16, 32, 64 or 128");
     pl->tb = static_cast<int>((M + pl->bn - 1) / pl->bn);
-    pl->split = o->mode == MQ_FAST && o->ksplit != 1;
+    pl->Mpad = int64_t(pl->tb) * pl->bn;
     pl->mode = o->mode == MQ_EXACT ? (pl->per_token ? kExactToken : kExactGroup) : (pl->per_token ? kFastToken : kFastGroup);
     pl->pdl = o->no_pdl == 0;
+    pl->rotate = o->mode == MQ_FAST;
+    pl->C = choose_cluster(L, *pl, o->ksplit);
+    const int64_t U1 = pl->C == 1 ? L->tiles8 + L->tiles4 : L->tiles8 + (L->tiles4 + 1) / 2;
+    pl->units = static_cast<int>(U1 * pl->tb);
     return MQ_OK;
 }
 
-// Every CTA must own at least one group: an empty range inside an item would
-// never arrive on the item's stream-K counter (the reduction counts the CTAs
-// ca..cz that overlap it). P <= X, so strictly increasing cuts always exist.
-void fill_cuts(GemmParams* p) {
-    const Schedule S(*p);
-    const int32_t X = static_cast<int32_t>(S.X);
-    for (int c = 0; c <= p->P; ++c) p->cuts[c] = static_cast<int32_t>(S.cut(c));
-    for (int c = 1; c < p->P; ++c) p->cuts[c] = std::max(p->cuts[c], p->cuts[c - 1] + 1);
-    for (int c = p->P - 1; c >= 1; --c) p->cuts[c] = std::min(p->cuts[c], p->cuts[c + 1] - 1);
-    p->cuts[0] = 0;
-    p->cuts[p->P] = X;
+// Engine activation layout (EAL) workspace: codes [G][Mpad][128] | scales [Ga][Mpad]
+struct EalWs {
+    size_t off_sa, total;
+};
+EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
+    EalWs w;
+    w.off_sa = size_t(L->G) * size_t(pl.Mpad) * 128;
+    const int64_t Ga = pl.per_token ? 1 : L->G;
+    w.total = w.off_sa + (size_t(Ga) * size_t(pl.Mpad) * 4 + 255) / 256 * 256;
+    return w;
 }
 
-// The launch grid and the stream-K cost weights (bytes streamed per group,
-// incl. the activation tile and a fixed per-group pipeline cost).
-void fill_schedule(const mq_layer_s* L, const Plan& pl, int sms, GemmParams* p) {
-    const int64_t items = (L->tiles8 + L->tiles4) * pl.tb;
-    const int64_t X = items * L->G;
-    p->split = pl.split ? 1 : 0;
-    p->P = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>({int64_t(sms), int64_t(kMaxCtas), pl.split ? X : items})));
-    p->c8 = (kBlock8Bytes + 128 * pl.bn + 1024) / 64;
-    p->c4 = (kBlock4Bytes + 128 * pl.bn + 1024) / 64;
-    fill_cuts(p);
-}
-
-size_t ws_bytes_for(const mq_layer_s* L, const Plan& pl, int sms) {
-    const int64_t items = (L->tiles8 + L->tiles4) * pl.tb;
-    const int64_t X = items * L->G;
-    const int64_t P = std::max<int64_t>(1, std::min<int64_t>(sms, pl.split ? X : items));
-    const size_t counters = ((size_t(items) * 4 + 255) / 256) * 256;
-    return counters + (pl.split ? size_t(2 * P) * 128 * pl.bn * 4 : 0);
-}
-
-// Activation codes as a 3-D tensor {128 (k in group), M, G} with byte strides
-// {ldc, 128}: one box {128, BN, GPS} lands GPS per-group [BN][128] SW128 tiles.
-// Scales (group-major [G][lds] f32) as 2-D {M, G}: box {BN, GPS}.
-mq_status encode_maps(CUtensorMap* amap, CUtensorMap* smap, const int8_t* codes, int64_t ldc, const float* scales,
-                      int64_t lds, int64_t M, int G, int bn, bool with_scales) {
-    auto fn = encode_fn();
-    if (!fn) return fail(MQ_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
-    const int gps = gemm_gps(bn);
-    {
-        const cuuint64_t dims[3] = {128u, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(G)};
-        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldc), 128u};
-        const cuuint32_t box[3] = {128u, static_cast<cuuint32_t>(bn), static_cast<cuuint32_t>(gps)};
-        const cuuint32_t estr[3] = {1u, 1u, 1u};
-        CUresult r = fn(amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(codes), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(MQ_CUDA, "cuTensorMapEncodeTiled(codes) failed: " + std::to_string(int(r)));
-    }
-    std::memset(smap, 0, sizeof(*smap));
-    if (with_scales) {
-        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(G)};
-        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(lds) * 4u};
-        const cuuint32_t box[2] = {static_cast<cuuint32_t>(bn), static_cast<cuuint32_t>(gps)};
-        const cuuint32_t estr[2] = {1u, 1u};
-        CUresult r = fn(smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(scales), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(MQ_CUDA, "cuTensorMapEncodeTiled(scales) failed: " + std::to_string(int(r)));
-    }
-    return MQ_OK;
-}
-
-void gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t lds, int64_t M, void* Y,
-                 mq_dtype out_dtype, void* ws, GemmParams* p) {
+void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dtype out_dtype, GemmParams* p) {
     std::memset(p, 0, sizeof(*p));
     p->T8 = static_cast<int32_t>(L->tiles8);
     p->T4 = static_cast<int32_t>(L->tiles4);
@@ -179,19 +141,14 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, const float* sa, int64_t l
     p->K = L->K;
     p->wq = L->d_wq;
     p->colmap = L->d_colmap;
-    p->sa = sa;
-    p->sa_gstride = pl.per_token ? 0 : lds;
+    p->Mpad = pl.Mpad;
     p->M = M;
     p->Y = Y;
     p->out_dtype = out_dtype;
     p->ldy = L->world > 1 ? L->shard_cols : L->N;
-    fill_schedule(L, pl, L->num_sms, p);
-    if (ws) {
-        const int64_t items = (L->tiles8 + L->tiles4) * pl.tb;
-        uint8_t* w = static_cast<uint8_t*>(ws);
-        p->counters = reinterpret_cast<uint32_t*>(w);
-        p->ws = reinterpret_cast<float*>(w + ((size_t(items) * 4 + 255) / 256) * 256);
-    }
+    p->C = pl.C;
+    p->units = pl.units;
+    p->rotate = pl.rotate ? 1 : 0;
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
     static const int dbg = [] {
         const char* e = std::getenv("MQ_DBG");
@@ -225,24 +182,6 @@ mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, cudaStream_t stream, v
     }
     *ws = L->d_ws;
     return MQ_OK;
-}
-
-int64_t lds_for(int64_t M) { return (M + 3) / 4 * 4; }
-
-// workspace of the full dynamic path: codes [M, ldc] | scales [Ga, lds] | gemm
-struct FullWs {
-    int64_t ldc, lds;
-    size_t off_scales, off_gemm, total;
-};
-FullWs full_ws_layout(const mq_layer_s* L, int64_t M, int per_token, size_t gemm_bytes) {
-    FullWs f;
-    f.ldc = (L->K + 127) / 128 * 128;
-    f.lds = lds_for(M);
-    const int64_t Ga = per_token ? 1 : L->G;
-    f.off_scales = size_t((M * f.ldc + 255) / 256 * 256);
-    f.off_gemm = f.off_scales + size_t((Ga * f.lds * 4 + 255) / 256 * 256);
-    f.total = f.off_gemm + gemm_bytes;
-    return f;
 }
 
 }  // namespace
@@ -421,8 +360,21 @@ mq_status mq_quantize_act(const void* A, mq_dtype dt, int64_t M, int64_t K, int6
 size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
     Plan pl;
     if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK) return 0;
-    return ws_bytes_for(L, pl, L->num_sms);
+    return eal_ws_layout(L, pl).total;
 }
+
+namespace {
+mq_status launch_k2(mq_layer_s* L, const Plan& pl, const uint8_t* acts, const float* sa, int64_t M, void* Y,
+                    mq_dtype out_dtype, cudaStream_t s) {
+    GemmParams p;
+    gemm_params(L, pl, M, Y, out_dtype, &p);
+    p.acts = acts;
+    p.sa = sa;
+    cudaError_t e = launch_mixed_gemm_tc(p, pl.bn, pl.mode, pl.pdl, s);
+    if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
+    return MQ_OK;
+}
+}  // namespace
 
 mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, const float* scales, int64_t lds,
                                 int64_t M, void* Y, mq_dtype out_dtype, const mq_exec_opts* o, void* ws,
@@ -430,76 +382,118 @@ mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, 
     if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
     if (M == 0) return MQ_OK;
-    if (ldc < int64_t(L->G) * kGroupK || ldc % 16 != 0)
-        return fail(MQ_USAGE, "ldc must be >= ceil(K/128)*128 (zero-padded columns) and a multiple of 16");
-    if (reinterpret_cast<uintptr_t>(codes) % 16 != 0) return fail(MQ_USAGE, "codes must be 16-byte aligned");
-    if (reinterpret_cast<uintptr_t>(scales) % 16 != 0) return fail(MQ_USAGE, "scales must be 16-byte aligned");
+    if (ldc < L->K) return fail(MQ_USAGE, "ldc must be >= K");
     if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
     Plan pl;
     if (mq_status st = make_plan(L, M, o, &pl)) return st;
-    if (!pl.per_token && (lds < M || lds % 4 != 0))
-        return fail(MQ_USAGE, "group-wise scales need lds >= M and lds % 4 == 0 (group-major layout)");
+    if (!pl.per_token && lds < M) return fail(MQ_USAGE, "group-wise scales need lds >= M (group-major layout)");
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (o && o->gemm_impl == 1) {
         GemmParams p;
-        gemm_params(L, pl, scales, lds, M, Y, out_dtype, nullptr, &p);
+        gemm_params(L, pl, M, Y, out_dtype, &p);
+        p.sa_rm = scales;
+        p.sa_gstride = pl.per_token ? 0 : lds;
         cudaError_t e = launch_mixed_gemm_simt(p, codes, ldc, pl.mode == kFastToken ? kFastToken : kExactGroup,
                                                L->w8_mode == MQ_W8_REFERENCE, s);
         if (e != cudaSuccess) return cuda_fail(e, "simt launch");
         return MQ_OK;
     }
-    const size_t need = ws_bytes_for(L, pl, L->num_sms);
+    const EalWs w = eal_ws_layout(L, pl);
     if (!ws) {
-        if (mq_status st = ensure_internal_ws(L, need, s, &ws)) return st;
+        if (mq_status st = ensure_internal_ws(L, w.total, s, &ws)) return st;
     }
-    GemmParams p;
-    gemm_params(L, pl, scales, lds, M, Y, out_dtype, ws, &p);
-    alignas(64) CUtensorMap amap, smap;
-    if (mq_status st = encode_maps(&amap, &smap, codes, ldc, scales, lds, M, L->G, pl.bn, !pl.per_token)) return st;
-    cudaError_t e = launch_mixed_gemm_tc(p, &amap, &smap, pl.bn, pl.mode, pl.pdl, s);
-    if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
-    return MQ_OK;
+    uint8_t* acts = static_cast<uint8_t*>(ws);
+    float* sa = reinterpret_cast<float*>(acts + w.off_sa);
+    cudaError_t e = launch_repack_eal(codes, ldc, scales, lds, pl.per_token, M, L->K, pl.Mpad, acts, sa, s);
+    if (e != cudaSuccess) return cuda_fail(e, "repack launch");
+    return launch_k2(L, pl, acts, sa, M, Y, out_dtype, s);
 }
 
 size_t mq_mixed_linear_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
-    Plan pl;
-    if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK) return 0;
-    return full_ws_layout(L, M, pl.per_token, mq_forward_workspace_bytes(L, M, o)).total;
+    return mq_forward_workspace_bytes(L, M, o);
 }
 
 mq_status mq_mixed_linear(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t M, void* Y, mq_dtype out_dtype,
                           const mq_exec_opts* o, void* ws, int32_t* err, void* stream) {
     if (!L) return fail(MQ_USAGE, "layer handle is null");
+    if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
     if (M == 0) return MQ_OK;
+    if (a_dtype != MQ_F32 && a_dtype != MQ_F16 && a_dtype != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
+    if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
     Plan pl;
     if (mq_status st = make_plan(L, M, o, &pl)) return st;
-    const FullWs f = full_ws_layout(L, M, pl.per_token, mq_forward_workspace_bytes(L, M, o));
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const EalWs w = eal_ws_layout(L, pl);
     if (!ws) {
-        if (mq_status st = ensure_internal_ws(L, f.total, static_cast<cudaStream_t>(stream), &ws)) return st;
+        if (mq_status st = ensure_internal_ws(L, w.total, s, &ws)) return st;
     }
-    uint8_t* w = static_cast<uint8_t*>(ws);
-    int8_t* codes = reinterpret_cast<int8_t*>(w);
-    float* scales = reinterpret_cast<float*>(w + f.off_scales);
-    const int32_t ag = pl.per_token ? int32_t(L->K) : int32_t(L->group);
-    if (a_dtype != MQ_F32 && a_dtype != MQ_F16 && a_dtype != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
-    cudaError_t e = launch_act_quant(A, a_dtype, M, L->K, L->K, ag, 0, codes, f.ldc, scales, f.lds, err, pl.pdl,
-                                     static_cast<cudaStream_t>(stream));
+    uint8_t* acts = static_cast<uint8_t*>(ws);
+    float* sa = reinterpret_cast<float*>(acts + w.off_sa);
+    if (o && o->gemm_impl == 1) return fail(MQ_USAGE, "the SIMT debug kernel takes quantized codes (mq_mixed_linear_codes)");
+    cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad, acts,
+                                         sa, err, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
-    return mq_mixed_linear_codes(L, codes, f.ldc, scales, f.lds, M, Y, out_dtype, o, w + f.off_gemm, stream);
+    return launch_k2(L, pl, acts, sa, M, Y, out_dtype, s);
+}
+
+mq_status mq_quantize_act_ws(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t M, const mq_exec_opts* o, void* ws,
+                             int32_t* err, void* stream) {
+    if (!L || !ws) return fail(MQ_USAGE, "layer handle / workspace is null");
+    if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
+    if (M == 0) return MQ_OK;
+    if (a_dtype != MQ_F32 && a_dtype != MQ_F16 && a_dtype != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
+    Plan pl;
+    if (mq_status st = make_plan(L, M, o, &pl)) return st;
+    const EalWs w = eal_ws_layout(L, pl);
+    uint8_t* acts = static_cast<uint8_t*>(ws);
+    cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad, acts,
+                                         reinterpret_cast<float*>(acts + w.off_sa), err, pl.pdl,
+                                         static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
+    return MQ_OK;
+}
+
+mq_status mq_mixed_linear_ws(mq_layer_t L, int64_t M, const void* ws, void* Y, mq_dtype out_dtype,
+                             const mq_exec_opts* o, void* stream) {
+    if (!L || !ws) return fail(MQ_USAGE, "layer handle / workspace is null");
+    if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
+    if (M == 0) return MQ_OK;
+    if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
+    Plan pl;
+    if (mq_status st = make_plan(L, M, o, &pl)) return st;
+    const EalWs w = eal_ws_layout(L, pl);
+    const uint8_t* acts = static_cast<const uint8_t*>(ws);
+    return launch_k2(L, pl, acts, reinterpret_cast<const float*>(acts + w.off_sa), M, Y, out_dtype,
+                     static_cast<cudaStream_t>(stream));
 }
 
 mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64_t M, int32_t which, int32_t* partials,
                            void* stream) {
     if (!L) return fail(MQ_USAGE, "layer handle is null");
     if (which != 0 && which != 1) return fail(MQ_USAGE, "which must be 0 (sub8) or 1 (sub4)");
-    if (ldc < int64_t(L->G) * kGroupK || ldc % 16 != 0)
-        return fail(MQ_USAGE, "ldc must be >= ceil(K/128)*128 (zero-padded columns) and a multiple of 16");
+    if (ldc < L->K) return fail(MQ_USAGE, "ldc must be >= K");
     if (M == 0) return MQ_OK;
+    mq_exec_opts o{};
+    o.mode = MQ_EXACT;
+    o.ksplit = 1;
     Plan pl;
-    if (mq_status st = make_plan(L, M, nullptr, &pl)) return st;
-    pl.split = false;
+    if (mq_status st = make_plan(L, M, &o, &pl)) return st;
+    pl.mode = kDumpPartials;
+    pl.rotate = false;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const EalWs w = eal_ws_layout(L, pl);
+    void* ws = nullptr;
+    if (mq_status st = ensure_internal_ws(L, w.total, s, &ws)) return st;
+    uint8_t* acts = static_cast<uint8_t*>(ws);
+    float* sa = reinterpret_cast<float*>(acts + w.off_sa);
+    // scales are unused by the dump: repack with zero scales from a null-free buffer
+    cudaError_t e = cudaMemsetAsync(sa, 0, w.total - w.off_sa, s);
+    if (e == cudaSuccess) e = launch_repack_eal(codes, ldc, sa, 0, 1, M, L->K, pl.Mpad, acts, sa, s);
+    if (e != cudaSuccess) return cuda_fail(e, "repack launch");
     GemmParams p;
-    gemm_params(L, pl, nullptr, 0, M, nullptr, MQ_F32, nullptr, &p);
+    gemm_params(L, pl, M, nullptr, MQ_F32, &p);
+    p.acts = acts;
+    p.sa = sa;
     // restrict the launch to one sub-problem: its tiles, offsets and rows
     if (which == 0) {
         p.T4 = 0;
@@ -511,13 +505,10 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
         p.n8 = 0;
     }
     if (p.T8 + p.T4 == 0) return MQ_OK;
-    p.P = static_cast<int32_t>(std::min<int64_t>({int64_t(L->num_sms), int64_t(kMaxCtas), int64_t(p.T8 + p.T4) * pl.tb}));
-    fill_cuts(&p);
+    p.units = (p.T8 + p.T4) * pl.tb;
     p.partials = partials;
     p.partial_rows = static_cast<int32_t>(which == 0 ? L->n8 : L->n4);
-    alignas(64) CUtensorMap amap, smap;
-    if (mq_status st = encode_maps(&amap, &smap, codes, ldc, nullptr, 0, M, L->G, pl.bn, false)) return st;
-    cudaError_t e = launch_mixed_gemm_tc(p, &amap, &smap, pl.bn, kDumpPartials, false, static_cast<cudaStream_t>(stream));
+    e = launch_mixed_gemm_tc(p, pl.bn, kDumpPartials, false, s);
     if (e != cudaSuccess) return cuda_fail(e, "partials launch");
     return MQ_OK;
 }

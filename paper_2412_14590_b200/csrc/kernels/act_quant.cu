@@ -13,6 +13,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <climits>
 
 #include "mq_kernels.hpp"
@@ -122,6 +123,133 @@ __global__ void __launch_bounds__(256) act_quant_row_kernel(
     if (threadIdx.x == 0) scales[m] = s;
 }
 
+// ----------------------------------------------------------------------------
+// EAL variants (mq_kernels.hpp): the same arithmetic, written straight into the
+// engine's tiled, pre-swizzled operand layout so K2 streams each chunk's
+// activations with one bulk copy. One warp per (token row m < Mpad, group g):
+// lane l owns codes [4l, 4l+4) of the group and stores them as one 32-bit word.
+template <int DT>
+__global__ void act_quant_eal_group_kernel(const void* __restrict__ A, int64_t M, int64_t K, int64_t lda, int G,
+                                           int64_t Mpad, uint8_t* __restrict__ acts, float* __restrict__ sa,
+                                           int32_t* err) {
+    griddep_wait();
+    griddep_launch();
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= Mpad * G) return;
+    const int g = static_cast<int>(wid / Mpad);
+    const int64_t m = wid - int64_t(g) * Mpad;
+    const int64_t b = int64_t(g) * 128;
+    const int len = static_cast<int>(K - b < 128 ? K - b : 128);
+    float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float amax = 0.0f;
+    bool finite = true;
+    if (m < M) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int k = 4 * lane + i;
+            if (k < len) {
+                x[i] = load_act<DT>(A, m * lda + b + k);
+                finite &= isfinite(x[i]);
+                amax = fmaxf(amax, fabsf(x[i]));
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    finite = __all_sync(0xffffffffu, finite);
+    uint32_t word = 0;
+    float s = 0.0f;
+    if (m < M) {
+        if (!finite && lane == 0 && err) atomicMin(err, static_cast<int32_t>(m * G + g));
+        s = act_scale(amax, 0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (4 * lane + i < len) word |= uint32_t(uint8_t(quant_one(x[i], s))) << (8 * i);
+    }
+    *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(4 * lane))) = word;
+    if (lane == 0) sa[int64_t(g) * Mpad + m] = s;
+}
+
+// per-token (group == K): one CTA per token row m < Mpad
+template <int DT>
+__global__ void __launch_bounds__(256) act_quant_eal_row_kernel(const void* __restrict__ A, int64_t M, int64_t K,
+                                                                int64_t lda, int G, int64_t Mpad,
+                                                                uint8_t* __restrict__ acts, float* __restrict__ sa,
+                                                                int32_t* err) {
+    griddep_wait();
+    griddep_launch();
+    __shared__ float red[8];
+    __shared__ int bad[8];
+    const int64_t m = blockIdx.x;
+    const bool live = m < M;
+    float amax = 0.0f;
+    bool finite = true;
+    if (live)
+        for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+            const float x = load_act<DT>(A, m * lda + i);
+            finite &= isfinite(x);
+            amax = fmaxf(amax, fabsf(x));
+        }
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const bool wfin = __all_sync(0xffffffffu, finite);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[w] = amax;
+        bad[w] = !wfin;
+    }
+    __syncthreads();
+    amax = red[0];
+    int anybad = bad[0];
+    for (int i = 1; i < 8; ++i) {
+        amax = fmaxf(amax, red[i]);
+        anybad |= bad[i];
+    }
+    if (live && anybad && threadIdx.x == 0 && err) atomicMin(err, static_cast<int32_t>(m));
+    const float s = live ? act_scale(amax, 0) : 0.0f;
+    // 4 codes per thread-iteration, all G groups of this row
+    for (int64_t q = threadIdx.x; q < int64_t(G) * 32; q += blockDim.x) {
+        const int g = static_cast<int>(q >> 5);
+        const int k0 = static_cast<int>(q & 31) * 4;
+        uint32_t word = 0;
+        if (live)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t k = int64_t(g) * 128 + k0 + i;
+                if (k < K) word |= uint32_t(uint8_t(quant_one(load_act<DT>(A, m * lda + k), s))) << (8 * i);
+            }
+        *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(k0))) = word;
+    }
+    if (threadIdx.x == 0) sa[m] = s;
+}
+
+// row-major codes/scales (reference layout) -> EAL; one thread per 4 codes
+__global__ void repack_eal_kernel(const int8_t* __restrict__ codes, int64_t ldc, const float* __restrict__ scales,
+                                  int64_t lds, int per_token, int64_t M, int64_t K, int G, int64_t Mpad,
+                                  uint8_t* __restrict__ acts, float* __restrict__ sa) {
+    const int64_t total = int64_t(G) * Mpad * 32;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(i / (Mpad * 32));
+        const int64_t rem = i - int64_t(g) * Mpad * 32;
+        const int64_t m = rem >> 5;
+        const int k0 = static_cast<int>(rem & 31) * 4;
+        uint32_t word = 0;
+        if (m < M)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t k = int64_t(g) * 128 + k0 + j;
+                if (k < K) word |= uint32_t(uint8_t(codes[m * ldc + k])) << (8 * j);
+            }
+        *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(k0))) = word;
+        if (k0 == 0) {
+            if (per_token) {
+                if (g == 0) sa[m] = m < M ? scales[m] : 0.0f;
+            } else {
+                sa[int64_t(g) * Mpad + m] = m < M ? scales[int64_t(g) * lds + m] : 0.0f;
+            }
+        }
+    }
+}
+
 template <typename K, typename... Args>
 cudaError_t launch_ex(K kern, dim3 grid, dim3 block, bool pdl, cudaStream_t stream, Args... args) {
     cudaLaunchConfig_t cfg{};
@@ -137,6 +265,38 @@ cudaError_t launch_ex(K kern, dim3 grid, dim3 block, bool pdl, cudaStream_t stre
 }
 
 }  // namespace
+
+cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda, int group,
+                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* err, bool pdl,
+                                 cudaStream_t stream) {
+    if (Mpad == 0) return cudaSuccess;
+    const int G = static_cast<int>((K + 127) / 128);
+    if (group >= K) {
+        const dim3 grid(static_cast<unsigned>(Mpad));
+        switch (a_dtype) {
+            case 0: return launch_ex(act_quant_eal_row_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+            case 1: return launch_ex(act_quant_eal_row_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+            default: return launch_ex(act_quant_eal_row_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+        }
+    }
+    const int64_t warps = Mpad * G;
+    const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));
+    switch (a_dtype) {
+        case 0: return launch_ex(act_quant_eal_group_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+        case 1: return launch_ex(act_quant_eal_group_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+        default: return launch_ex(act_quant_eal_group_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+    }
+}
+
+cudaError_t launch_repack_eal(const int8_t* codes, int64_t ldc, const float* scales, int64_t lds, int per_token,
+                              int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, cudaStream_t stream) {
+    const int G = static_cast<int>((K + 127) / 128);
+    const int64_t total = int64_t(G) * Mpad * 32;
+    if (total == 0) return cudaSuccess;
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
+    repack_eal_kernel<<<grid, 256, 0, stream>>>(codes, ldc, scales, lds, per_token, M, K, G, Mpad, acts, sa);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_act_quant(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda,
                              int group, int f16, int8_t* codes, int64_t ldc, float* scales,

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(128) mixed_gemm_simt_kernel(const GemmParams p
             if (mode == kFastToken) {
                 acc[t] = __fmaf_rn(gs, sw, acc[t]);
             } else {
-                const float sa = p.sa[int64_t(g) * p.sa_gstride + m];
+                const float sa = p.sa_rm[int64_t(g) * p.sa_gstride + m];
                 acc[t] = __fadd_rn(acc[t], __fmul_rn(gs, __fmul_rn(sa, sw)));
             }
         }
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(128) mixed_gemm_simt_kernel(const GemmParams p
         const int64_t m = m0 + t;
         if (m >= p.M) break;
         float v = acc[t];
-        if (mode == kFastToken) v = __fmul_rn(v, p.sa[m]);
+        if (mode == kFastToken) v = __fmul_rn(v, p.sa_rm[m]);
         store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
     }
 }

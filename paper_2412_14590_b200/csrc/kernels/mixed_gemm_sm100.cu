@@ -8,30 +8,34 @@
 // and the two sub-problems (8-bit / 4-bit output features) are scattered back
 // to their original columns (proj/src/mixed.cpp:83-120).
 //
-// B200 design: one persistent warp-specialised kernel over both sub-problems;
-// CTA c owns the stream-K range [cuts[c], cuts[c+1]) of linearised
-// (tile, token block, K-group) work (mq_kernels.hpp). Work moves in CHUNKS of
-// up to GPS consecutive groups of one tile (GPS/2 for sub8); every hand-off
-// between roles is per chunk, not per group (mbarrier round trips dominate
-// at decode sizes):
+// B200 design. One launch covers both sub-problems (the paper's "parallel
+// sub-problems"). Each CTA owns one (128-row weight tile,
+// token tile, K-slice) — see work_of() in mq_kernels.hpp: K-slices of one tile
+// live in one thread-block CLUSTER and are reduced in fixed order through
+// distributed shared memory, so split-K needs no global workspace and stays
+// deterministic. Work moves in CHUNKS of up to GPS consecutive groups (GPS/2 for
+// sub8, whose groups are twice the bytes); roles are warp-specialised and hand
+// off per chunk through mbarriers:
 //   warp 0      producer: per chunk one cp.async.bulk of the merged code+meta
-//               blocks (L2 evict-first), one 3-D TMA of the chunk's int8
-//               activation tiles (SWIZZLE_128B), one 2-D TMA of its activation
-//               scales; the first NS weight copies issue BEFORE
-//               griddepcontrol.wait so under PDL they overlap the previous kernel;
-//   converter   (sub4) one thread per weight row: 4 conflict-free 16-B loads,
-//               nibbles -> int8 (c - z) with the carry-free bias trick
-//               ((x & 0x0F0F0F0F) + (128 - z)*0x01010101) ^ 0x80808080 — the
-//               paper's step-1 zero-point subtraction — and a
-//               tcgen05.st of the row straight into a TMEM A-operand ring;
+//               blocks (L2 evict-first) and one bulk copy each of the chunk's
+//               activation tiles / scales, which K1 already wrote in the
+//               engine activation layout (EAL, pre-swizzled SW128 images). The
+//               first NS weight copies issue BEFORE griddepcontrol.wait, so under
+//               PDL they overlap the previous kernel;
+//   converter   one thread per weight row: sub4 nibbles -> int8 (c - z) with the
+//               carry-free bias trick ((x & 0x0F0F0F0F) + (128 - z)*0x01010101) ^
+//               0x80808080 (the paper's step-1 zero-point subtraction,
+//               PAPER.md:344-353), tcgen05.st of the row into a TMEM A-operand
+//               ring; for every chunk it also copies the weight / activation
+//               scales into a small meta ring, so a stage is released as soon as
+//               the converter and the MMA are done with it;
 //   warp 1      TMEM allocation, then MMA issue (elected lane): 4 x tcgen05.mma
-//               (K = 32) per group, A from TMEM (sub4) or from the
-//               pre-swizzled SMEM block (sub8), each group into a fresh int32
-//               TMEM accumulator;
-//   epilogue    tcgen05.ld the group sums, exact int->float (I2FP), rescale and
-//               accumulate in f32 registers (step 2), then scatter the tile to
-//               the original output columns (f32/f16/bf16) or publish a
-//               stream-K partial (last arriver reduces in fixed order).
+//               (K = 32) per group, A from TMEM (sub4) or from the pre-swizzled
+//               SMEM block (sub8), each group into a fresh int32 TMEM accumulator;
+//   epilogue    tcgen05.ld the group sums, exact int->float, rescale and
+//               accumulate in f32 registers (step 2); at the end scatter to the
+//               original output columns (f32/f16/bf16), through the cluster's
+//               DSMEM reduction when the tile is split along K.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -57,14 +61,14 @@ struct TcCfg {
     // columns, NA A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
     static constexpr int NT = BN >= 128 ? 3 : 2;
-    static constexpr int NA = int((512u - NT * kAccPerChunk) / kAPerChunk) > 4 ? 4 : int((512u - NT * kAccPerChunk) / kAPerChunk);
+    static constexpr int NA0 = int((512u - NT * kAccPerChunk) / kAPerChunk);
+    static constexpr int NA = NA0 > 4 ? 4 : NA0;
     static constexpr uint32_t kAccCols = NT * kAccPerChunk;
     static constexpr uint32_t kACol0 = kAccCols;
     static constexpr uint32_t kTmemNeed = kAccCols + NA * kAPerChunk;
     static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
     static_assert(kTmemNeed <= 512 && NA >= 2, "TMEM budget");
-    // meta ring (per accumulator slot): weight scales [GPS][128] + act scales [GPS][BN],
-    // copied out of the stage by the converter so stages free up before the epilogue runs
+    // meta ring (per accumulator slot): weight scales [GPS][128] + act scales [GPS][BN]
     static constexpr int kMetaSlot = GPS * (128 + BN) * 4;
     static constexpr int kMetaBytes = NT * kMetaSlot;
     static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/ + kMetaBytes;
@@ -81,10 +85,19 @@ struct TcCfg {
     static constexpr int kSmem = kFixed + NS * kStageBytes;
     static_assert(NS >= 2, "pipeline needs at least two stages");
     static_assert(GPS * BN <= 128, "act-scale copy: one converter thread per value");
+    static_assert(128 * BN * 4 <= NS * kStageBytes, "split-K reduction buffer lives in the stage ring");
 };
 
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+// f32 load from CTA `rank`'s shared memory at the same offset as local address `a`
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t a, uint32_t rank) {
+    uint32_t ra;
+    float v;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+    return v;
 }
 // one lane of a converged warp (elect.sync): keeps tcgen05/TMA operands warp-uniform
 __device__ __forceinline__ bool elect_one() {
@@ -98,7 +111,7 @@ __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.
 __device__ __forceinline__ void trace(const GemmParams& p, int ev) {
     if (p.trace) {
         unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
         p.trace[blockIdx.x * 8 + ev] = t;
     }
 }
@@ -127,24 +140,6 @@ struct Ring {
     }
 };
 
-// One contiguous run of K-groups of one work item inside this CTA's range.
-struct Seg {
-    int32_t x0;  // linear index of the first group
-    int32_t item;
-    int tile, tb, g0, g1;
-};
-__device__ __forceinline__ Seg seg_at(const GemmParams& p, int32_t x, int32_t xe) {
-    Seg s;
-    s.x0 = x;
-    s.item = x / p.G;
-    s.g0 = x - s.item * p.G;
-    const int32_t end = (s.item + 1) * p.G;
-    s.g1 = s.g0 + ((end < xe ? end : xe) - x);
-    s.tile = s.item / p.TB;
-    s.tb = s.item - s.tile * p.TB;
-    return s;
-}
-
 // nibbles of one packed word -> two words of int8 (c - z): codes 0..3 and 4..7
 __device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& lo, uint32_t& hi) {
     lo = ((w & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
@@ -152,9 +147,7 @@ __device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& l
 }
 
 template <int BN, int MODE>
-__global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1)
-mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_constant__ CUtensorMap tmap_sa,
-                     const __grid_constant__ GemmParams p) {
+__global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(const __grid_constant__ GemmParams p) {
     using C = TcCfg<BN>;
     constexpr int NS = C::NS, NE = C::NE, BNE = C::BNE, GPS = C::GPS, NA = C::NA, NT = C::NT, NC = C::NC;
     constexpr bool kSa = (MODE == kExactGroup || MODE == kFastGroup);
@@ -174,7 +167,6 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
     uint64_t* mfull = tempty + NT;         // [NT] converter -> epilogue (meta slot written)
     uint64_t* tmem_ready = mfull + NT;     // warp 1 -> everyone using TMEM
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_ready + 1);
-    int* last_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto stage = [&](int s) { return stages + s * C::kStageBytes; };
@@ -200,33 +192,26 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
     if (threadIdx.x == 0) trace(p, 0);
     griddep_launch();  // let the next kernel in the stream start its prologue
 
-    const int32_t xb = p.cuts[blockIdx.x], xe = p.cuts[blockIdx.x + 1];
-
-    // Every role walks this CTA's work as the same sequence of (segment, chunk)
-    // pairs; f(sg, ti, gc, cg) runs once per chunk and returns false to stop.
-    auto for_chunks = [&](auto&& f) {
-        for (int32_t x = xb; x < xe;) {
-            const Seg sg = seg_at(p, x, xe);
-            x += sg.g1 - sg.g0;
-            const TileInfo ti = tile_info(p, sg.tile);
-            const int gps = ti.is8 ? C::GPS8 : GPS;
-            for (int gc = sg.g0; gc < sg.g1; gc += gps) {
-                const int cg = (sg.g1 - gc) < gps ? (sg.g1 - gc) : gps;
-                if (!f(sg, ti, gc, cg)) return;
-            }
-        }
+    const Work wk = work_of(p, blockIdx.x);
+    const bool live = wk.tile >= 0;
+    const TileInfo ti = tile_info(p, live ? wk.tile : 0);
+    const int gps = ti.is8 ? C::GPS8 : GPS;
+    const int nch = live ? (wk.g1 - wk.g0 + gps - 1) / gps : 0;
+    // FAST modes start each CTA at a different chunk of its K-slice so the CTAs
+    // of a launch do not all read the same activation lines at the same time
+    const int rot = (p.rotate && nch > 1) ? int((blockIdx.x * 7u) % uint32_t(nch)) : 0;
+    auto chunk_at = [&](int i, int& gc, int& cg) {
+        int c = i + rot;
+        if (c >= nch) c -= nch;
+        gc = wk.g0 + c * gps;
+        cg = (wk.g1 - gc) < gps ? (wk.g1 - gc) : gps;
     };
 
     if (warp == 0) {
         // ============================== producer ==============================
-        if (elect_one()) {
-            ptx::prefetch_tmap(&tmap_act);
-            if (kSa) ptx::prefetch_tmap(&tmap_sa);
-        }
         const uint64_t pol_w = ptx::policy_evict_first();
         const uint64_t pol_a = ptx::policy_evict_last();
-        constexpr uint32_t kBBytes = GPS * BN * 128;  // full boxes (OOB rows / groups zero-filled)
-        constexpr uint32_t kSaBytes = kSa ? GPS * BN * 4 : 0;
+        const bool contig = p.Mpad == BN;  // one token tile: a chunk's act tiles are contiguous
         // pass 0: weights of the first NS chunks (independent of the previous
         // kernel); pass 1: activations/scales + everything else.
         for (int pass = 0; pass < 2; ++pass) {
@@ -236,32 +221,46 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                 if (lane == 0) trace(p, 2);
             }
             Ring rr;
-            int n = 0;
-            for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
+            for (int n = 0; n < nch; ++n) {
                 const bool pre = n < NS;
-                if (pass == 0 && !pre) return false;
+                if (pass == 0 && !pre) break;
+                int gc, cg;
+                chunk_at(n, gc, cg);
                 uint8_t* st = stage(rr.idx);
                 if (pass == 0 || !pre) {
                     if (pass == 1) ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
                     if (lane == 0) trace_chunk(p, 0, n);
                     const uint32_t wbytes = uint32_t(cg * ti.blk);
+                    const uint32_t abytes = uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0));
                     if (elect_one()) {
-                        ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes + kBBytes + kSaBytes);
+                        ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes + abytes);
                         ptx::bulk_g2s(st, p.wq + ti.off + int64_t(gc) * ti.blk, wbytes, &full[rr.idx], pol_w);
                     }
                     __syncwarp();
                 }
                 if (pass == 1) {
                     if (elect_one()) {
-                        ptx::tma_load_3d(st + C::kOffB, &tmap_act, 0, sg.tb * BN, gc, &full[rr.idx], pol_a);
-                        if (kSa) ptx::tma_load_2d(st + C::kOffSa, &tmap_sa, sg.tb * BN, gc, &full[rr.idx], pol_a);
+                        const int64_t row0 = int64_t(wk.tb) * BN;
+                        if (contig) {
+                            ptx::bulk_g2s(st + C::kOffB, p.acts + int64_t(gc) * p.Mpad * 128, uint32_t(cg * BN * 128),
+                                          &full[rr.idx], pol_a);
+                            if (kSa)
+                                ptx::bulk_g2s(st + C::kOffSa, p.sa + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4),
+                                              &full[rr.idx], pol_a);
+                        } else {
+                            for (int j = 0; j < cg; ++j) {
+                                ptx::bulk_g2s(st + C::kOffB + j * BN * 128, p.acts + (int64_t(gc + j) * p.Mpad + row0) * 128,
+                                              uint32_t(BN * 128), &full[rr.idx], pol_a);
+                                if (kSa)
+                                    ptx::bulk_g2s(st + C::kOffSa + j * BN * 4, p.sa + int64_t(gc + j) * p.Mpad + row0,
+                                                  uint32_t(BN * 4), &full[rr.idx], pol_a);
+                            }
+                        }
                     }
                     __syncwarp();
                 }
                 rr.next<NS>();
-                ++n;
-                return true;
-            });
+            }
         }
     } else if (warp == 1) {
         // ======================= TMEM allocation + MMA issuer ==================
@@ -274,13 +273,14 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
         const uint32_t idesc4 = idesc_i8(BN, true, true);
         const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
         Ring rs, ra, rt;
-        int nch = 0;
-        for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
+        for (int n = 0; n < nch; ++n) {
+            int gc, cg;
+            chunk_at(n, gc, cg);
             ptx::mbar_wait(&full[rs.idx], rs.ph);
             ptx::mbar_wait(&afull[ra.idx], ra.ph);
             ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
             ptx::tc_fence_after();
-            if (lane == 0) trace_chunk(p, 1, nch);
+            if (lane == 0) trace_chunk(p, 1, n);
             const uint32_t st = ptx::smem_u32(stage(rs.idx));
             if (elect_one()) {
                 if (!(p.dbg & 4)) {
@@ -307,31 +307,30 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                 ptx::tc_commit(&empty[rs.idx]);
             }
             __syncwarp();
-            if (lane == 0) trace_chunk(p, 2, nch++);
+            if (lane == 0) trace_chunk(p, 2, n);
             ra.next<NA>();
             rt.next<NT>();
             rs.next<NS>();
-            return true;
-        });
+        }
     } else if (warp >= 4 && warp < 4 + 4 * NC) {
-        // =================== converter (sub4 -> int8 A tiles in TMEM) ===================
-        const int wg = (warp - 4) >> 2;   // converter warpgroup: takes groups j = wg, wg+NC, ...
+        // ============ converter (sub4 -> int8 A tiles in TMEM; scales -> meta ring) ============
+        const int wg = (warp - 4) >> 2;        // converter warpgroup: takes groups j = wg, wg+NC, ...
         const int r = (warp & 3) * 32 + lane;  // weight row = TMEM lane
         ptx::mbar_wait(tmem_ready, 0);
         ptx::tc_fence_after();
         const uint32_t tmem_row = *reinterpret_cast<volatile uint32_t*>(tmem_holder) + (uint32_t((warp & 3) * 32) << 16);
         Ring rs, ra, rt;
-        int nch = 0;
-        for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
+        for (int n = 0; n < nch; ++n) {
+            int gc, cg;
+            chunk_at(n, gc, cg);
             // every chunk (sub8 too): wait for the stage, a free A slot and a free
-            // meta slot, then (sub4) convert codes into TMEM and (all) copy the
-            // chunk's weight / activation scales into the meta ring, so the stage
-            // is released by the converter + MMA, never by the epilogue.
+            // meta slot (a role that skipped chunks could run two phases ahead of
+            // a barrier and read an older phase's parity as complete)
             ptx::mbar_wait(&full[rs.idx], rs.ph);
-            if (threadIdx.x == 128) trace_chunk(p, 5, nch);
+            if (threadIdx.x == 128) trace_chunk(p, 5, n);
             ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
             ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
-            if (threadIdx.x == 128) trace_chunk(p, 6, nch);
+            if (threadIdx.x == 128) trace_chunk(p, 6, n);
             const uint8_t* st = stage(rs.idx);
             float* msw = meta + rt.idx * (C::kMetaSlot / 4);
             for (int j = wg; j < cg; j += NC) {
@@ -353,8 +352,7 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                     msw[j * 128 + r] = reinterpret_cast<const float*>(st + j * kBlock8Bytes + kCodes8Bytes)[r];
                 }
             }
-            if (kSa && wg == 0 && r < cg * BN)
-                msw[GPS * 128 + r] = reinterpret_cast<const float*>(st + C::kOffSa)[r];
+            if (kSa && wg == 0 && r < cg * BN) msw[GPS * 128 + r] = reinterpret_cast<const float*>(st + C::kOffSa)[r];
             if (!ti.is8) ptx::tmem_wait_st();
             ptx::tc_fence_before();
             __syncwarp();
@@ -363,46 +361,43 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
                 ptx::mbar_arrive(&afull[ra.idx]);
                 ptx::mbar_arrive(&empty[rs.idx]);
             }
-            if (threadIdx.x == 128) trace_chunk(p, 3, nch);
-            ++nch;
+            if (threadIdx.x == 128) trace_chunk(p, 3, n);
             ra.next<NA>();
             rt.next<NT>();
             rs.next<NS>();
-            return true;
-        });
-    } else if (int(threadIdx.x) >= C::kEpiThread0) {
-        // ============================== epilogue ==============================
-        const int et = threadIdx.x - C::kEpiThread0;  // 0 .. 128*NE-1
-        const int e = et >> 7;                        // epilogue warpgroup
-        const int wq = warp & 3;                      // TMEM lane quarter this warp may access
-        const int r = wq * 32 + lane;                 // tile row (= TMEM lane)
-        const int c0 = e * BNE;                       // first token column of this warpgroup
+        }
+    }
+
+    // ================================ epilogue ================================
+    const bool is_epi = int(threadIdx.x) >= C::kEpiThread0;
+    const int et = threadIdx.x - C::kEpiThread0;  // 0 .. 128*NE-1
+    const int e = et >> 7;                        // epilogue warpgroup
+    const int wq = warp & 3;                      // TMEM lane quarter this warp may access
+    const int r = wq * 32 + lane;                 // tile row (= TMEM lane)
+    const int c0 = e * BNE;                       // first token column of this warpgroup
+    const int64_t m0 = int64_t(wk.tb) * BN + c0;  // first token of this warpgroup
+    if (is_epi) {
+        float acc[BNE];
+#pragma unroll
+        for (int j = 0; j < BNE; ++j) acc[j] = 0.0f;
+        float sat[MODE == kExactToken ? BNE : 1];  // per-token s_a of this warpgroup's tokens
         ptx::mbar_wait(tmem_ready, 0);
         ptx::tc_fence_after();
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
-        griddep_wait();  // workspace / scales / output of this launch are ours now
+        griddep_wait();  // scales / output of this launch are ours now
+        if constexpr (MODE == kExactToken) {
+#pragma unroll
+            for (int j = 0; j < BNE; ++j) sat[j] = m0 + j < p.M ? __ldg(p.sa + m0 + j) : 0.0f;
+        }
         Ring rt;
-        bool first_group = true;
-        float acc[BNE];
-        float sat[MODE == kExactToken ? BNE : 1];  // per-token s_a of this warpgroup's tokens
-        int nch = 0;
-        for_chunks([&](const Seg& sg, const TileInfo& ti, int gc, int cg) {
-            if (gc == sg.g0) {
-#pragma unroll
-                for (int j = 0; j < BNE; ++j) acc[j] = 0.0f;
-                if constexpr (MODE == kExactToken) {
-                    const int64_t mb = int64_t(sg.tb) * BN + c0;
-#pragma unroll
-                    for (int j = 0; j < BNE; ++j) sat[j] = mb + j < p.M ? __ldg(p.sa + mb + j) : 0.0f;
-                }
-            }
+        for (int n = 0; n < nch; ++n) {
+            int gc, cg;
+            chunk_at(n, gc, cg);
             ptx::mbar_wait(&mfull[rt.idx], rt.ph);
             ptx::mbar_wait(&tfull[rt.idx], rt.ph);
             ptx::tc_fence_after();
-            if (first_group && et == 0) trace(p, 3);
-            first_group = false;
+            if (n == 0 && et == 0) trace(p, 3);
             const float* msw = meta + rt.idx * (C::kMetaSlot / 4);
-            const int64_t m0 = int64_t(sg.tb) * BN + c0;  // first token of this warpgroup
             for (int j = 0; j < cg; ++j) {
                 const float sw = msw[j * 128 + r];
                 const float* sav = msw + GPS * 128 + j * BN + c0;
@@ -444,70 +439,55 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[rt.idx]);
-            if (et == 0) trace_chunk(p, 4, nch);
-            ++nch;
+            if (et == 0) trace_chunk(p, 4, n);
             rt.next<NT>();
-            if (gc + cg < sg.g1) return true;  // the segment continues in the next chunk
-
-            // ---------------- end of segment: output or stream-K partial
-            if constexpr (MODE == kDumpPartials) return true;
-            if (et == 0) trace(p, 4);
-            const int col = r < ti.rows ? __ldg(p.colmap + sg.tile * kTileRows + r) : -1;
-            bool do_store = true;
-            const int32_t xs = sg.item * p.G;  // the item's linear group range [xs, xs + G)
-            if (p.split && !(xb <= xs && xe >= xs + p.G)) {
-                // this CTA holds only part of the item: publish the partial tile to
-                // slot 2*c + (first segment of this CTA ? 0 : 1); the last arriving
-                // CTA sums the item's partials in CTA order (deterministic).
-                const int slot = 2 * int(blockIdx.x) + (sg.x0 == xb ? 0 : 1);
-                float* part = p.ws + (int64_t(slot) * 128 + r) * BN + c0;
+        }
+        if (et == 0) trace(p, 4);
+        if (MODE != kDumpPartials && live) {
+            if (wk.S == 1) {
+                // whole-K tile: scatter straight to the original output columns
+                const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
+                if (col >= 0) {
 #pragma unroll
-                for (int j = 0; j < BNE; j += 4)
-                    __stcg(reinterpret_cast<float4*>(part + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
-                __threadfence();
-                named_bar_sync(3, 128 * NE);
-                const int ca = cta_owner(p, xs), cz = cta_owner(p, xs + p.G - 1);
-                if (et == 0) {
-                    const uint32_t prev = atomicAdd(p.counters + sg.item, 1u);
-                    *reinterpret_cast<volatile int*>(last_flag) = (prev == uint32_t(cz - ca));
-                }
-                named_bar_sync(3, 128 * NE);
-                do_store = *reinterpret_cast<volatile int*>(last_flag) != 0;
-                if (do_store) {
-                    __threadfence();
-                    const bool ca_first = p.cuts[ca] == xs;
-                    for (int k = ca; k <= cz; ++k) {
-                        const int sk = 2 * k + ((k == ca && !ca_first) ? 1 : 0);
-                        const float* src = p.ws + (int64_t(sk) * 128 + r) * BN + c0;
-#pragma unroll
-                        for (int j = 0; j < BNE; j += 4) {
-                            const float4 t = __ldcg(reinterpret_cast<const float4*>(src + j));
-                            if (k == ca) {
-                                acc[j] = t.x; acc[j + 1] = t.y; acc[j + 2] = t.z; acc[j + 3] = t.w;
-                            } else {
-                                acc[j] = __fadd_rn(acc[j], t.x);
-                                acc[j + 1] = __fadd_rn(acc[j + 1], t.y);
-                                acc[j + 2] = __fadd_rn(acc[j + 2], t.z);
-                                acc[j + 3] = __fadd_rn(acc[j + 3], t.w);
-                            }
+                    for (int j = 0; j < BNE; ++j) {
+                        const int64_t m = m0 + j;
+                        if (m < p.M) {
+                            float v = acc[j];
+                            if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
+                            store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
                         }
                     }
-                    if (et == 0) p.counters[sg.item] = 0u;  // re-arm for the next launch
                 }
-            }
-            if (do_store && col >= 0) {
+            } else {
+                // K-slice partial -> own smem [BN][128] (the stage ring is drained), reduced below
+                float* red = reinterpret_cast<float*>(stages);
 #pragma unroll
-                for (int j = 0; j < BNE; ++j) {
-                    const int64_t m = m0 + j;
-                    if (m < p.M) {
-                        float v = acc[j];
-                        if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                        store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
-                    }
+                for (int j = 0; j < BNE; ++j) red[(c0 + j) * 128 + r] = acc[j];
+            }
+        }
+    }
+
+    if (p.C > 1) {
+        // Cluster split-K: every K-slice CTA of an item reduces rows
+        // [sl*128/S, (sl+1)*128/S) of the item's tile over its S slices, in
+        // slice order (deterministic), and scatters them.
+        cluster_sync_all();
+        if (is_epi && live && MODE != kDumpPartials && wk.S > 1) {
+            const int rb = (wk.sl * 128) / wk.S, re = ((wk.sl + 1) * 128) / wk.S, nr = re - rb;
+            const uint32_t red_base = ptx::smem_u32(stages);
+            for (int q = et; q < nr * BN; q += 128 * NE) {
+                const int tok = q / nr, row = rb + q - tok * nr;
+                const uint32_t a = red_base + uint32_t((tok * 128 + row) * 4);
+                float v = ld_dsmem_f32(a, uint32_t(wk.rank0));
+                for (int s = 1; s < wk.S; ++s) v = __fadd_rn(v, ld_dsmem_f32(a, uint32_t(wk.rank0 + s)));
+                const int64_t m = int64_t(wk.tb) * BN + tok;
+                if (row < ti.rows && m < p.M) {
+                    if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
+                    store_out(p.Y, p.out_dtype, m * p.ldy + __ldg(p.colmap + wk.tile * kTileRows + row), v);
                 }
             }
-            return true;
-        });
+        }
+        cluster_sync_all();  // peers' partial tiles stay alive until every reader is done
     }
 
     if (threadIdx.x == C::kEpiThread0) trace(p, 5);
@@ -521,7 +501,7 @@ mixed_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_act, const __grid_
 }
 
 template <int BN, int MODE>
-cudaError_t launch_bn_mode(const GemmParams& p, const void* tmap, const void* tmap_sa, bool pdl, cudaStream_t stream) {
+cudaError_t launch_bn_mode(const GemmParams& p, bool pdl, cudaStream_t stream) {
     using C = TcCfg<BN>;
     auto kern = mixed_gemm_tc_kernel<BN, MODE>;
     static thread_local uint64_t configured = 0;  // per device ordinal bitmask
@@ -530,31 +510,69 @@ cudaError_t launch_bn_mode(const GemmParams& p, const void* tmap, const void* tm
     if (!(configured >> dev & 1)) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
         configured |= uint64_t(1) << dev;
     }
-    if (p.P <= 0) return cudaSuccess;
+    if (p.units <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.P);
+    cfg.gridDim = dim3(unsigned(p.units * p.C));
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (p.C > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = unsigned(p.C);
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, *static_cast<const CUtensorMap*>(tmap),
-                              *static_cast<const CUtensorMap*>(tmap_sa), p);
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int BN, int MODE>
+int max_clusters_bn_mode(int C) {
+    using Cfg = TcCfg<BN>;
+    auto kern = mixed_gemm_tc_kernel<BN, MODE>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(C * 64));
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
 }
 
 template <int BN>
-cudaError_t launch_bn(const GemmParams& p, const void* tmap, const void* tmap_sa, int mode, bool pdl, cudaStream_t s) {
+cudaError_t launch_bn(const GemmParams& p, int mode, bool pdl, cudaStream_t s) {
     switch (mode) {
-        case kExactGroup: return launch_bn_mode<BN, kExactGroup>(p, tmap, tmap_sa, pdl, s);
-        case kFastGroup: return launch_bn_mode<BN, kFastGroup>(p, tmap, tmap_sa, pdl, s);
-        case kFastToken: return launch_bn_mode<BN, kFastToken>(p, tmap, tmap_sa, pdl, s);
-        case kExactToken: return launch_bn_mode<BN, kExactToken>(p, tmap, tmap_sa, pdl, s);
-        default: return launch_bn_mode<BN, kDumpPartials>(p, tmap, tmap_sa, pdl, s);
+        case kExactGroup: return launch_bn_mode<BN, kExactGroup>(p, pdl, s);
+        case kFastGroup: return launch_bn_mode<BN, kFastGroup>(p, pdl, s);
+        case kFastToken: return launch_bn_mode<BN, kFastToken>(p, pdl, s);
+        case kExactToken: return launch_bn_mode<BN, kExactToken>(p, pdl, s);
+        default: return launch_bn_mode<BN, kDumpPartials>(p, pdl, s);
     }
 }
 
@@ -569,13 +587,22 @@ int gemm_stages(int bn) {
     }
 }
 
-cudaError_t launch_mixed_gemm_tc(const GemmParams& p, const void* tmap, const void* tmap_sa, int token_tile, int mode,
-                                 bool pdl, cudaStream_t stream) {
+int gemm_max_clusters(int token_tile, int mode, int C) {
+    const bool tok = mode == kFastToken;
     switch (token_tile) {
-        case 16: return launch_bn<16>(p, tmap, tmap_sa, mode, pdl, stream);
-        case 32: return launch_bn<32>(p, tmap, tmap_sa, mode, pdl, stream);
-        case 64: return launch_bn<64>(p, tmap, tmap_sa, mode, pdl, stream);
-        case 128: return launch_bn<128>(p, tmap, tmap_sa, mode, pdl, stream);
+        case 16: return tok ? max_clusters_bn_mode<16, kFastToken>(C) : max_clusters_bn_mode<16, kFastGroup>(C);
+        case 32: return tok ? max_clusters_bn_mode<32, kFastToken>(C) : max_clusters_bn_mode<32, kFastGroup>(C);
+        case 64: return tok ? max_clusters_bn_mode<64, kFastToken>(C) : max_clusters_bn_mode<64, kFastGroup>(C);
+        default: return tok ? max_clusters_bn_mode<128, kFastToken>(C) : max_clusters_bn_mode<128, kFastGroup>(C);
+    }
+}
+
+cudaError_t launch_mixed_gemm_tc(const GemmParams& p, int token_tile, int mode, bool pdl, cudaStream_t stream) {
+    switch (token_tile) {
+        case 16: return launch_bn<16>(p, mode, pdl, stream);
+        case 32: return launch_bn<32>(p, mode, pdl, stream);
+        case 64: return launch_bn<64>(p, mode, pdl, stream);
+        case 128: return launch_bn<128>(p, mode, pdl, stream);
         default: return cudaErrorInvalidValue;
     }
 }

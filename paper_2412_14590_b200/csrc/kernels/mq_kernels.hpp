@@ -9,21 +9,35 @@
 namespace mq {
 
 enum GemmMode : int {
-    kExactGroup = 0,  // reference op order (f32 mul then add), whole work items
-    kFastGroup = 1,   // FFMA rescale, group-wise s_a, stream-K splits
-    kFastToken = 2,   // per-token s_a factored out: acc += gs*s_w, y = s_a*acc
-    kDumpPartials = 3, // int32 group sums to a [G, M, rows] buffer
-    kExactToken = 4   // reference op order with a per-token s_a broadcast over groups
+    kExactGroup = 0,    // reference op order (f32 mul then add), no K splitting
+    kFastGroup = 1,     // FFMA rescale, group-wise s_a, cluster split-K
+    kFastToken = 2,     // per-token s_a factored out: acc += gs*s_w, y = s_a*acc
+    kDumpPartials = 3,  // int32 group sums to a [G, M, rows] buffer
+    kExactToken = 4     // reference op order with a per-token s_a broadcast over groups
 };
 
-// Everything the kernel needs is scalar: tile descriptors and the stream-K
-// schedule are recomputed arithmetically in every CTA (no dependent global
-// loads before the first weight copy). Work = items (tile, token block) x G
-// K-groups, linearised item-major with the sub8 tiles first; CTA c owns the
-// linear group range [cut(c), cut(c+1)) — cost-weighted (sub8 groups stream
-// ~2x the bytes of sub4 groups) when split, whole items otherwise.
-constexpr int kMaxCtas = 160;  // >= SM count (148 on B200)
+// ---------------------------------------------------------------------------
+// Engine activation layout (EAL), written by K1 and streamed by K2 with plain
+// bulk copies (one per chunk when the batch fits one token tile):
+//   codes  uint8 [G][Mpad][128]: byte (g, m, k) at g*Mpad*128 + m*128 +
+//          ((((k >> 4) ^ (m & 7)) << 4) | (k & 15))  — each (group, token-tile)
+//          is a ready UMMA K-major SWIZZLE_128B operand image;
+//   scales f32   [G][Mpad] (group-wise) or [Mpad] (per-token).
+// Mpad = TB * BN (token tile BN); rows m >= M are zero. Ragged K groups are
+// zero-padded to 128.
+__host__ __device__ inline uint32_t eal_offset(uint32_t m, uint32_t k) {
+    return m * 128u + ((((k >> 4) ^ (m & 7u)) << 4) | (k & 15u));
+}
 
+// ---------------------------------------------------------------------------
+// K2 schedule. A launch is a grid of UNITS x C CTAs in clusters of C:
+//   C == 1 ("plain"): a unit is one (tile, token block) over all K groups.
+//   C >= 2, even ("paired split-K"): a unit is either ONE sub8 tile split into
+//     C K-slices, or TWO sub4 tiles each split into C/2 K-slices — every CTA
+//     streams about the same bytes (a sub8 group is 2x a sub4 group). The
+//     K-slice partial tiles of an item are reduced in fixed order through
+//     distributed shared memory inside the cluster (deterministic, no global
+//     workspace). Units are ordered token-block-major, sub8 units first.
 struct GemmParams {
     int32_t T8, T4;         // 128-row tiles of sub8 / sub4
     int64_t n8, n4;         // rows of sub8 / sub4
@@ -32,48 +46,83 @@ struct GemmParams {
     int64_t K;
     const uint8_t* wq;      // merged code+meta blocks (mq_layout.cuh)
     const int32_t* colmap;  // [ (T8+T4)*128 ] output column of every tile row
-    const float* sa;        // activation scales, group-major: sa[g * sa_gstride + m]
-    int64_t sa_gstride;     // lds (group-wise) or 0 (per-token)
+    // EAL activations (tensor-core kernel)
+    const uint8_t* acts;    // [G][Mpad][128]
+    const float* sa;        // [G][Mpad] (group-wise) or [Mpad] (per-token)
+    int64_t Mpad;
+    // row-major activations (SIMT debug kernel): scales sa_rm[g * sa_gstride + m]
+    const float* sa_rm;
+    int64_t sa_gstride;
     int64_t M;
     void* Y;
     int32_t out_dtype;      // mq_dtype
     int64_t ldy;
-    int32_t P;              // CTAs
-    int32_t split;          // 1: stream-K (cuts inside items), 0: whole items
-    int32_t c8, c4;         // per-group stream costs (split mode)
-    float* ws;              // stream-K partial tiles [2*P][128][BN]
-    uint32_t* counters;     // arrival counters [items]
+    int32_t C;              // cluster size (1 = plain)
+    int32_t units;          // grid = units * C
+    int32_t rotate;         // 1: each CTA starts its K loop at a CTA-dependent chunk (FAST modes)
     uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int32_t* partials;      // dump mode
     int32_t partial_rows;
-    int32_t cuts[kMaxCtas + 1];  // CTA c owns linear groups [cuts[c], cuts[c+1]) (param space: no loads)
     int32_t dbg;            // development: pipeline-stage bypass bits (MQ_DBG env), 0 in production
     unsigned long long* trace;  // development: per-CTA globaltimer stamps [P][8] (MQ_DBG & 32)
 };
 
+// One CTA's work: rows of `tile` x tokens of block `tb` x groups [g0, g1);
+// the item's S K-slices sit on cluster ranks [rank0, rank0 + S), this CTA is
+// slice `sl`. tile < 0: idle CTA (odd sub4 tile count).
+struct Work {
+    int tile, tb, g0, g1, S, sl, rank0;
+};
+__host__ __device__ inline Work work_of(const GemmParams& p, int cta) {
+    Work w;
+    const int C = p.C;
+    const int unit = cta / C, s = cta - unit * C;
+    const int U1 = C == 1 ? p.T8 + p.T4 : p.T8 + (p.T4 + 1) / 2;  // units per token block
+    w.tb = unit / U1;
+    const int u = unit - w.tb * U1;
+    if (C == 1) {
+        w.tile = u, w.S = 1, w.sl = 0, w.rank0 = 0;
+    } else if (u < p.T8) {
+        w.tile = u, w.S = C, w.sl = s, w.rank0 = 0;
+    } else {
+        const int half = C / 2;
+        const int t4 = 2 * (u - p.T8) + s / half;
+        w.tile = t4 < p.T4 ? p.T8 + t4 : -1;
+        w.S = half, w.sl = s % half, w.rank0 = (s / half) * half;
+    }
+    w.g0 = int((int64_t(w.sl) * p.G) / w.S);
+    w.g1 = int((int64_t(w.sl + 1) * p.G) / w.S);
+    return w;
+}
+
 // tcgen05 product kernel. token_tile in {16,32,64,128}; mode per GemmMode;
-// tmap_act: 3-D tensor map {128, M, G} over the int8 codes (box {128, BN, GPS});
-// tmap_sa: 2-D tensor map {M, G} over the group-major scales (box {BN, GPS});
 // pdl = launch with programmatic stream serialization (prologue + weight
 // prefetch overlap the previous kernel).
-cudaError_t launch_mixed_gemm_tc(const GemmParams& p, const void* tmap_act, const void* tmap_sa, int token_tile,
-                                 int mode, bool pdl, cudaStream_t stream);
+cudaError_t launch_mixed_gemm_tc(const GemmParams& p, int token_tile, int mode, bool pdl, cudaStream_t stream);
 // groups of a sub4 tile per pipeline stage (sub8: half) for a token tile
 #ifndef MQ_GPS_SMALL
 #define MQ_GPS_SMALL 4
 #endif
 constexpr int gemm_gps(int token_tile) { return token_tile <= 32 ? MQ_GPS_SMALL : (token_tile == 64 ? 2 : 1); }
 int gemm_stages(int token_tile);
-// SIMT debug kernel (same layout, exact op order); parity aid, not the product.
+// how many clusters of C CTAs of the (FAST-mode) kernel can be co-resident (cudaOccupancyMaxActiveClusters)
+int gemm_max_clusters(int token_tile, int mode, int C);
+// SIMT debug kernel (same weight layout, exact op order, row-major activations).
 cudaError_t launch_mixed_gemm_simt(const GemmParams& p, const int8_t* codes, int64_t ldc,
                                    int mode, int w8_unsigned, cudaStream_t stream);
-// K1. scales are written group-major: scales[g * lds + m] (per-token: scales[m]).
+// K1 (reference layout): codes [M, ldc] row-major; scales group-major scales[g * lds + m] (per-token: scales[m]).
 cudaError_t launch_act_quant(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda,
                              int group, int f16_scales, int8_t* codes, int64_t ldc, float* scales,
                              int64_t lds, int32_t* err, bool pdl, cudaStream_t stream);
-cudaError_t launch_permute(const void* gathered, const int32_t* colmap, int world,
-                           int64_t shard_cols, int64_t M, int64_t N, void* Y, int dtype,
-                           cudaStream_t stream);
+// K1 (engine layout, EAL): group == 128 (group-wise) or K (per-token).
+cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda, int group,
+                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* err, bool pdl,
+                                 cudaStream_t stream);
+// Row-major codes [M, ldc] + group-major scales [G, lds] (or [M]) -> EAL.
+cudaError_t launch_repack_eal(const int8_t* codes, int64_t ldc, const float* scales, int64_t lds, int per_token,
+                              int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, cudaStream_t stream);
+cudaError_t launch_permute(const void* gathered, const int32_t* colmap, int world, int64_t shard_cols,
+                           int64_t M, int64_t N, void* Y, int dtype, cudaStream_t stream);
 
 // Tile descriptor of tile t (sub8 tiles first), identical to the host packer.
 struct TileInfo {
@@ -100,50 +149,5 @@ __host__ __device__ inline TileInfo tile_info(const GemmParams& p, int t) {
     }
     return ti;
 }
-
-// CTA owning linear group x (binary search over the parameter-space cut table).
-__host__ __device__ inline int cta_owner(const GemmParams& p, int32_t x) {
-    int lo = 0, hi = p.P - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (p.cuts[mid] <= x) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
-// The stream-K partition (see GemmParams); evaluated once on the host to fill
-// GemmParams::cuts.
-struct Schedule {
-    int64_t X8, X, U, items;
-    int32_t G, P, split, c8, c4;
-    __host__ __device__ Schedule(const GemmParams& p) {
-        items = int64_t(p.T8 + p.T4) * p.TB;
-        X8 = int64_t(p.T8) * p.TB * p.G;
-        X = items * p.G;
-        G = p.G;
-        P = p.P;
-        split = p.split;
-        c8 = p.c8;
-        c4 = p.c4;
-        U = X8 * c8 + (X - X8) * c4;
-    }
-    __host__ __device__ int64_t cut(int c) const {
-        if (c <= 0) return 0;
-        if (c >= P) return X;
-        if (!split) return (int64_t(c) * items / P) * G;
-        const int64_t t = (U / P) * c + ((U % P) * c) / P;  // floor(U*c/P) without overflow
-        const int64_t x = t <= X8 * c8 ? (t + c8 - 1) / c8 : X8 + (t - X8 * c8 + c4 - 1) / c4;
-        return x < X ? x : X;
-    }
-    __host__ __device__ int cta_of(int64_t x) const {  // the CTA whose range holds x (split mode)
-        const int64_t cx = x <= X8 ? x * c8 : X8 * c8 + (x - X8) * c4;
-        int c = int((cx * P) / (U > 0 ? U : 1));
-        if (c > P - 1) c = P - 1;
-        while (c > 0 && cut(c) > x) --c;
-        while (c < P - 1 && cut(c + 1) <= x) ++c;
-        return c;
-    }
-};
 
 }  // namespace mq

@@ -300,6 +300,10 @@ class DeviceLayer:
         M = A.shape[0]
         if out is None:
             out = torch.empty((M, self.out_cols), dtype=out_dtype or torch.float32, device=A.device)
+        if opts.gemm_impl == 1:  # SIMT debug kernel: takes reference-layout codes
+            ag = opts.act_group or self.info.group_size
+            codes, scales = quantize_act(A, ag, err=err, stream=stream)
+            return self.forward_codes(codes, scales, out=out, opts=opts, stream=stream)
         ws = workspace if workspace is not None else self.workspace(M, opts, True)
         check(lib().mq_mixed_linear(self.h, _p(A), _dt(A), M, _p(out), _dt(out), C.byref(opts), _p(ws),
                                     _p(err), _stream(stream)))
@@ -318,6 +322,24 @@ class DeviceLayer:
         lds = scales.stride(0) if scales.dim() == 2 else scales.numel()
         check(lib().mq_mixed_linear_codes(self.h, _p(codes), codes.stride(0), _p(scales), lds, M, _p(out),
                                           _dt(out), C.byref(opts), _p(ws), _stream(stream)))
+        return out
+
+    def quantize_ws(self, A, opts: capi.mq_exec_opts | None = None, err=None, stream=None, workspace=None):
+        """K1 into the engine activation layout inside a workspace (mq_quantize_act_ws);
+        returns the workspace, to be consumed by forward_ws (one or many layers)."""
+        opts = opts or exec_opts()
+        ws = workspace if workspace is not None else self.workspace(A.shape[0], opts, True)
+        check(lib().mq_quantize_act_ws(self.h, _p(A), _dt(A), A.shape[0], C.byref(opts), _p(ws), _p(err),
+                                       _stream(stream)))
+        return ws
+
+    def forward_ws(self, M: int, ws, out=None, out_dtype=None, opts: capi.mq_exec_opts | None = None, stream=None):
+        """K2 alone on activations quantize_ws left in `ws` (mq_mixed_linear_ws)."""
+        import torch
+        opts = opts or exec_opts()
+        if out is None:
+            out = torch.empty((M, self.out_cols), dtype=out_dtype or torch.float32, device=ws.device)
+        check(lib().mq_mixed_linear_ws(self.h, M, _p(ws), _p(out), _dt(out), C.byref(opts), _stream(stream)))
         return out
 
     def partials(self, codes, which: int, stream=None):

@@ -9,14 +9,14 @@ L = mq.partition_and_quantize(W, prom)
 reps = 4
 layers = [mq.DeviceLayer(L) for _ in range(reps)]
 dA = torch.from_numpy(A).cuda()
-codes, scales = mq.quantize_act(dA, 128)
 Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
 opts = mq.exec_opts(capi.MQ_FAST, 128, ksplit=int(os.environ.get("KSPLIT", "0")))
-for dl in layers: dl.forward_codes(codes, scales, out=Y, opts=opts)
+ws = layers[0].quantize_ws(dA, opts)
+for dl in layers: dl.forward_ws(M, ws, out=Y, opts=opts)
 torch.cuda.synchronize()
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g):
-    for i in range(20): layers[i % reps].forward_codes(codes, scales, out=Y, opts=opts)
+    for i in range(20): layers[i % reps].forward_ws(M, ws, out=Y, opts=opts)
 g.replay(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()

@@ -8,13 +8,13 @@ W, A, prom = mq.bench_inputs(M, N, K, 0.1, 1)
 L = mq.partition_and_quantize(W, prom)
 dl = mq.DeviceLayer(L)
 dA = torch.from_numpy(A).cuda()
-codes, scales = mq.quantize_act(dA, 128)
 Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
 opts = mq.exec_opts(capi.MQ_FAST, 128, pdl=False, ksplit=int(os.environ.get("KSPLIT", "0")))
-for _ in range(3): dl.forward_codes(codes, scales, out=Y, opts=opts)
+ws = dl.quantize_ws(dA, opts)
+for _ in range(3): dl.forward_ws(M, ws, out=Y, opts=opts)
 torch.cuda.synchronize()
 t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
-t0.record(); dl.forward_codes(codes, scales, out=Y, opts=opts); t1.record(); torch.cuda.synchronize()
+t0.record(); dl.forward_ws(M, ws, out=Y, opts=opts); t1.record(); torch.cuda.synchronize()
 print("event us", t0.elapsed_time(t1) * 1e3)
 buf = (C.c_ulonglong * (148 * 8 + 1024))()
 n = capi.lib().mq_debug_trace(buf)

@@ -16,15 +16,15 @@ def bench(n, k, m, mode, act_group=128, iters=50, reps=8, token_tile=0, ksplit=0
     layers = [mq.DeviceLayer(L) for _ in range(reps)]  # rotate > L2 for big shapes
     dA = torch.from_numpy(A).cuda()
     opts = mq.exec_opts(mode, act_group, ksplit=ksplit, token_tile=token_tile)
-    codes, scales = mq.quantize_act(dA, act_group)
+    ws = layers[0].quantize_ws(dA, opts)
     Y = torch.empty((m, n), dtype=torch.float16, device="cuda")
     for dl in layers:
-        dl.forward_codes(codes, scales, out=Y, opts=opts)
+        dl.forward_ws(m, ws, out=Y, opts=opts)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(iters):
-        layers[i % reps].forward_codes(codes, scales, out=Y, opts=opts)
+        layers[i % reps].forward_ws(m, ws, out=Y, opts=opts)
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / iters * 1e3
