@@ -64,32 +64,27 @@ int auto_token_tile(int64_t M) {
 }
 
 struct Plan {
-    int bn, tb, mode, per_token, C, units;
+    int bn, tb, mode, per_token, S4, S8, ctas;
     int64_t Mpad;
     bool pdl, rotate;
 };
 
-// Cluster size of the paired split-K schedule (mq_kernels.hpp): the largest
-// even C <= 8 whose grid still fits in one wave of co-resident clusters; at
-// decode sizes the K-slices keep every SM streaming. Exact mode keeps the
-// reference's ascending group order per output, so it never splits.
-int choose_cluster(const mq_layer_s* L, const Plan& pl, int ksplit) {
-    if (pl.mode == kExactGroup || pl.mode == kExactToken || ksplit == 1) return 1;
-    if (ksplit >= 2) return std::min(8, ksplit & ~1);
-    const int64_t U1 = L->tiles8 + (L->tiles4 + 1) / 2;
-    if (pl.tb > 1) return 1;  // token-tiled (prefill) launches are tensor-bound: one tile per CTA
-    static thread_local int cache[4][2][9] = {};  // [bn][token mode][C] -> co-resident clusters (+1)
-    const int bi = pl.bn == 16 ? 0 : pl.bn == 32 ? 1 : pl.bn == 64 ? 2 : 3, ti = pl.mode == kFastToken;
-    int best = 2;
-    for (int C = 8; C >= 2; C -= 2) {
-        int& n = cache[bi][ti][C];
-        if (n == 0) n = 1 + gemm_max_clusters(pl.bn, pl.mode, C);
-        if (n > 1 && U1 * pl.tb <= int64_t(n - 1)) {
-            best = C;
-            break;
-        }
+// K-slices per item (mq_kernels.hpp schedule). Exact mode keeps the
+// reference's ascending group order per output, so it never splits; token-
+// tiled (prefill) launches are tensor-bound and use one tile per CTA. Decode
+// splits sub4 tiles S ways and sub8 tiles 2S ways (equal bytes per CTA), S as
+// large as one wave of SMs allows.
+void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
+    pl->S4 = pl->S8 = 1;
+    if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1) return;
+    int S = ksplit >= 2 ? ksplit : 1;
+    if (ksplit == 0) {
+        const int64_t base = 2 * L->tiles8 + L->tiles4;
+        S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, L->num_sms / std::max<int64_t>(base, 1))));
     }
-    return best;
+    S = std::max(1, std::min(S, L->G / 2));
+    pl->S4 = S;
+    pl->S8 = std::min(2 * S, std::max(1, L->G));
 }
 
 mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
@@ -103,7 +98,7 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
                                   std::to_string(act_group) + ", weight group " + std::to_string(L->group) +
                                   "); per-token activations use act_group = K");
     if (o->mode != MQ_EXACT && o->mode != MQ_FAST) return fail(MQ_USAGE, "unknown mode");
-    if (o->ksplit < 0 || o->ksplit > 8) return fail(MQ_USAGE, "ksplit must be 0 (auto), 1 (none) or a cluster size <= 8");
+    if (o->ksplit < 0 || o->ksplit > 8) return fail(MQ_USAGE, "ksplit must be 0 (auto), 1 (none) or a split <= 8");
     pl->bn = o->token_tile ? o->token_tile : auto_token_tile(M);
     if (pl->bn != 16 && pl->bn != 32 && pl->bn != 64 && pl->bn != 128)
         return fail(MQ_USAGE, "token_tile must be 16, 32, 64 or 128");
@@ -112,21 +107,27 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     pl->mode = o->mode == MQ_EXACT ? (pl->per_token ? kExactToken : kExactGroup) : (pl->per_token ? kFastToken : kFastGroup);
     pl->pdl = o->no_pdl == 0;
     pl->rotate = o->mode == MQ_FAST;
-    pl->C = choose_cluster(L, *pl, o->ksplit);
-    const int64_t U1 = pl->C == 1 ? L->tiles8 + L->tiles4 : L->tiles8 + (L->tiles4 + 1) / 2;
-    pl->units = static_cast<int>(U1 * pl->tb);
+    choose_split(L, pl, o->ksplit);
+    pl->ctas = static_cast<int>((int64_t(pl->S8) * L->tiles8 + int64_t(pl->S4) * L->tiles4) * pl->tb);
     return MQ_OK;
 }
 
-// Engine activation layout (EAL) workspace: codes [G][Mpad][128] | scales [Ga][Mpad]
+// Forward workspace: split-K arrival counters (zero between launches; the
+// kernel re-arms them) | split-K partial tiles | EAL codes [G][Mpad][128] |
+// EAL scales [Ga][Mpad].
 struct EalWs {
-    size_t off_sa, total;
+    size_t off_part, off_acts, off_sa, total;
 };
 EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
     EalWs w;
-    w.off_sa = size_t(L->G) * size_t(pl.Mpad) * 128;
+    const size_t items = size_t(pl.tb) * size_t(L->tiles8 + L->tiles4);
+    w.off_part = al(items * 4);
+    const bool split = pl.S4 > 1 || pl.S8 > 1;
+    w.off_acts = w.off_part + (split ? al(size_t(pl.ctas) * 128 * size_t(pl.bn) * 4) : 0);
+    w.off_sa = w.off_acts + al(size_t(L->G) * size_t(pl.Mpad) * 128);
     const int64_t Ga = pl.per_token ? 1 : L->G;
-    w.total = w.off_sa + (size_t(Ga) * size_t(pl.Mpad) * 4 + 255) / 256 * 256;
+    w.total = w.off_sa + al(size_t(Ga) * size_t(pl.Mpad) * 4);
     return w;
 }
 
@@ -146,8 +147,9 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dty
     p->Y = Y;
     p->out_dtype = out_dtype;
     p->ldy = L->world > 1 ? L->shard_cols : L->N;
-    p->C = pl.C;
-    p->units = pl.units;
+    p->S4 = pl.S4;
+    p->S8 = pl.S8;
+    p->ctas = pl.ctas;
     p->rotate = pl.rotate ? 1 : 0;
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
     static const int dbg = [] {
@@ -364,12 +366,16 @@ size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o
 }
 
 namespace {
-mq_status launch_k2(mq_layer_s* L, const Plan& pl, const uint8_t* acts, const float* sa, int64_t M, void* Y,
-                    mq_dtype out_dtype, cudaStream_t s) {
+mq_status launch_k2(mq_layer_s* L, const Plan& pl, const void* ws, int64_t M, void* Y, mq_dtype out_dtype,
+                    cudaStream_t s) {
+    const EalWs w = eal_ws_layout(L, pl);
+    uint8_t* base = static_cast<uint8_t*>(const_cast<void*>(ws));
     GemmParams p;
     gemm_params(L, pl, M, Y, out_dtype, &p);
-    p.acts = acts;
-    p.sa = sa;
+    p.cnt = reinterpret_cast<uint32_t*>(base);
+    p.part = reinterpret_cast<float*>(base + w.off_part);
+    p.acts = base + w.off_acts;
+    p.sa = reinterpret_cast<const float*>(base + w.off_sa);
     cudaError_t e = launch_mixed_gemm_tc(p, pl.bn, pl.mode, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
     return MQ_OK;
@@ -402,11 +408,11 @@ mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, 
     if (!ws) {
         if (mq_status st = ensure_internal_ws(L, w.total, s, &ws)) return st;
     }
-    uint8_t* acts = static_cast<uint8_t*>(ws);
-    float* sa = reinterpret_cast<float*>(acts + w.off_sa);
+    uint8_t* acts = static_cast<uint8_t*>(ws) + w.off_acts;
+    float* sa = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + w.off_sa);
     cudaError_t e = launch_repack_eal(codes, ldc, scales, lds, pl.per_token, M, L->K, pl.Mpad, acts, sa, s);
     if (e != cudaSuccess) return cuda_fail(e, "repack launch");
-    return launch_k2(L, pl, acts, sa, M, Y, out_dtype, s);
+    return launch_k2(L, pl, ws, M, Y, out_dtype, s);
 }
 
 size_t mq_mixed_linear_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
@@ -427,13 +433,13 @@ mq_status mq_mixed_linear(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t
     if (!ws) {
         if (mq_status st = ensure_internal_ws(L, w.total, s, &ws)) return st;
     }
-    uint8_t* acts = static_cast<uint8_t*>(ws);
-    float* sa = reinterpret_cast<float*>(acts + w.off_sa);
+    uint8_t* acts = static_cast<uint8_t*>(ws) + w.off_acts;
+    float* sa = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + w.off_sa);
     if (o && o->gemm_impl == 1) return fail(MQ_USAGE, "the SIMT debug kernel takes quantized codes (mq_mixed_linear_codes)");
     cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad, acts,
                                          sa, err, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
-    return launch_k2(L, pl, acts, sa, M, Y, out_dtype, s);
+    return launch_k2(L, pl, ws, M, Y, out_dtype, s);
 }
 
 mq_status mq_quantize_act_ws(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t M, const mq_exec_opts* o, void* ws,
@@ -445,9 +451,9 @@ mq_status mq_quantize_act_ws(mq_layer_t L, const void* A, mq_dtype a_dtype, int6
     Plan pl;
     if (mq_status st = make_plan(L, M, o, &pl)) return st;
     const EalWs w = eal_ws_layout(L, pl);
-    uint8_t* acts = static_cast<uint8_t*>(ws);
-    cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad, acts,
-                                         reinterpret_cast<float*>(acts + w.off_sa), err, pl.pdl,
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad,
+                                         base + w.off_acts, reinterpret_cast<float*>(base + w.off_sa), err, pl.pdl,
                                          static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
     return MQ_OK;
@@ -461,10 +467,7 @@ mq_status mq_mixed_linear_ws(mq_layer_t L, int64_t M, const void* ws, void* Y, m
     if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
     Plan pl;
     if (mq_status st = make_plan(L, M, o, &pl)) return st;
-    const EalWs w = eal_ws_layout(L, pl);
-    const uint8_t* acts = static_cast<const uint8_t*>(ws);
-    return launch_k2(L, pl, acts, reinterpret_cast<const float*>(acts + w.off_sa), M, Y, out_dtype,
-                     static_cast<cudaStream_t>(stream));
+    return launch_k2(L, pl, ws, M, Y, out_dtype, static_cast<cudaStream_t>(stream));
 }
 
 mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64_t M, int32_t which, int32_t* partials,
@@ -484,8 +487,8 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
     const EalWs w = eal_ws_layout(L, pl);
     void* ws = nullptr;
     if (mq_status st = ensure_internal_ws(L, w.total, s, &ws)) return st;
-    uint8_t* acts = static_cast<uint8_t*>(ws);
-    float* sa = reinterpret_cast<float*>(acts + w.off_sa);
+    uint8_t* acts = static_cast<uint8_t*>(ws) + w.off_acts;
+    float* sa = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + w.off_sa);
     // scales are unused by the dump: repack with zero scales from a null-free buffer
     cudaError_t e = cudaMemsetAsync(sa, 0, w.total - w.off_sa, s);
     if (e == cudaSuccess) e = launch_repack_eal(codes, ldc, sa, 0, 1, M, L->K, pl.Mpad, acts, sa, s);
@@ -505,7 +508,8 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
         p.n8 = 0;
     }
     if (p.T8 + p.T4 == 0) return MQ_OK;
-    p.units = (p.T8 + p.T4) * pl.tb;
+    p.S4 = p.S8 = 1;
+    p.ctas = (p.T8 + p.T4) * pl.tb;
     p.partials = partials;
     p.partial_rows = static_cast<int32_t>(which == 0 ? L->n8 : L->n4);
     e = launch_mixed_gemm_tc(p, pl.bn, kDumpPartials, false, s);

@@ -10,10 +10,9 @@
 //
 // B200 design. One launch covers both sub-problems (the paper's "parallel
 // sub-problems"). Each CTA owns one (128-row weight tile,
-// token tile, K-slice) — see work_of() in mq_kernels.hpp: K-slices of one tile
-// live in one thread-block CLUSTER and are reduced in fixed order through
-// distributed shared memory, so split-K needs no global workspace and stays
-// deterministic. Work moves in CHUNKS of up to GPS consecutive groups (GPS/2 for
+// token tile, K-slice) — see work_of() in mq_kernels.hpp; the K-slices of a
+// split tile are reduced in slice order by the last one to finish
+// (deterministic). Work moves in CHUNKS of up to GPS consecutive groups (GPS/2 for
 // sub8, whose groups are twice the bytes); roles are warp-specialised and hand
 // off per chunk through mbarriers:
 //   warp 0      producer: per chunk one cp.async.bulk of the merged code+meta
@@ -34,8 +33,8 @@
 //               SMEM block (sub8), each group into a fresh int32 TMEM accumulator;
 //   epilogue    tcgen05.ld the group sums, exact int->float, rescale and
 //               accumulate in f32 registers (step 2); at the end scatter to the
-//               original output columns (f32/f16/bf16), through the cluster's
-//               DSMEM reduction when the tile is split along K.
+//               original output columns (f32/f16/bf16), through the split-K
+//               partial workspace when the tile is split along K.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -85,19 +84,10 @@ struct TcCfg {
     static constexpr int kSmem = kFixed + NS * kStageBytes;
     static_assert(NS >= 2, "pipeline needs at least two stages");
     static_assert(GPS * BN <= 128, "act-scale copy: one converter thread per value");
-    static_assert(128 * BN * 4 <= NS * kStageBytes, "split-K reduction buffer lives in the stage ring");
 };
 
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
-}
-// f32 load from CTA `rank`'s shared memory at the same offset as local address `a`
-__device__ __forceinline__ float ld_dsmem_f32(uint32_t a, uint32_t rank) {
-    uint32_t ra;
-    float v;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
-    return v;
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 // one lane of a converged warp (elect.sync): keeps tcgen05/TMA operands warp-uniform
 __device__ __forceinline__ bool elect_one() {
@@ -167,6 +157,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     uint64_t* mfull = tempty + NT;         // [NT] converter -> epilogue (meta slot written)
     uint64_t* tmem_ready = mfull + NT;     // warp 1 -> everyone using TMEM
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_ready + 1);
+    volatile int* s_last = reinterpret_cast<volatile int*>(tmem_holder + 1);  // split-K: this CTA reduces
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto stage = [&](int s) { return stages + s * C::kStageBytes; };
@@ -193,10 +184,10 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     griddep_launch();  // let the next kernel in the stream start its prologue
 
     const Work wk = work_of(p, blockIdx.x);
-    const bool live = wk.tile >= 0;
+    const bool live = true;
     const TileInfo ti = tile_info(p, live ? wk.tile : 0);
     const int gps = ti.is8 ? C::GPS8 : GPS;
-    const int nch = live ? (wk.g1 - wk.g0 + gps - 1) / gps : 0;
+    const int nch = (live && !(p.dbg & 8)) ? (wk.g1 - wk.g0 + gps - 1) / gps : 0;  // dbg&8: launch-floor probe
     // FAST modes start each CTA at a different chunk of its K-slice so the CTAs
     // of a launch do not all read the same activation lines at the same time
     const int rot = (p.rotate && nch > 1) ? int((blockIdx.x * 7u) % uint32_t(nch)) : 0;
@@ -264,7 +255,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         }
     } else if (warp == 1) {
         // ======================= TMEM allocation + MMA issuer ==================
-        ptx::tmem_alloc<C::kTmemCols>(tmem_holder);
+        if (!(p.dbg & 16)) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);  // dbg&16 (with &8): launch-floor probe
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(tmem_ready);
@@ -459,42 +450,53 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                     }
                 }
             } else {
-                // K-slice partial -> own smem [BN][128] (the stage ring is drained), reduced below
-                float* red = reinterpret_cast<float*>(stages);
+                // split-K: publish this slice's partial tile, count arrivals; the
+                // last slice sums all S partials in slice order and scatters them
+                float* mine = p.part + int64_t(blockIdx.x) * (BN * 128);
 #pragma unroll
-                for (int j = 0; j < BNE; ++j) red[(c0 + j) * 128 + r] = acc[j];
-            }
-        }
-    }
-
-    if (p.C > 1) {
-        // Cluster split-K: every K-slice CTA of an item reduces rows
-        // [sl*128/S, (sl+1)*128/S) of the item's tile over its S slices, in
-        // slice order (deterministic), and scatters them.
-        cluster_sync_all();
-        if (is_epi && live && MODE != kDumpPartials && wk.S > 1) {
-            const int rb = (wk.sl * 128) / wk.S, re = ((wk.sl + 1) * 128) / wk.S, nr = re - rb;
-            const uint32_t red_base = ptx::smem_u32(stages);
-            for (int q = et; q < nr * BN; q += 128 * NE) {
-                const int tok = q / nr, row = rb + q - tok * nr;
-                const uint32_t a = red_base + uint32_t((tok * 128 + row) * 4);
-                float v = ld_dsmem_f32(a, uint32_t(wk.rank0));
-                for (int s = 1; s < wk.S; ++s) v = __fadd_rn(v, ld_dsmem_f32(a, uint32_t(wk.rank0 + s)));
-                const int64_t m = int64_t(wk.tb) * BN + tok;
-                if (row < ti.rows && m < p.M) {
-                    if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                    store_out(p.Y, p.out_dtype, m * p.ldy + __ldg(p.colmap + wk.tile * kTileRows + row), v);
+                for (int j = 0; j < BNE; ++j) __stcg(mine + (c0 + j) * 128 + r, acc[j]);
+                named_bar_sync(2, 128 * NE);
+                if (et == 0) {
+                    __threadfence();
+                    const uint32_t prev = atomicAdd(p.cnt + wk.item, 1u);
+                    *s_last = prev == uint32_t(wk.S - 1);
+                    if (prev == uint32_t(wk.S - 1)) p.cnt[wk.item] = 0u;  // re-arm for the next launch
+                }
+                named_bar_sync(2, 128 * NE);
+                if (*s_last) {
+                    __threadfence();
+                    const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
+                    const float* base = p.part + int64_t(wk.cta0) * (BN * 128) + c0 * 128 + r;
+                    for (int j0 = 0; j0 < BNE; j0 += 4) {
+                        float t[4][16];
+#pragma unroll
+                        for (int s2 = 0; s2 < 16; ++s2)
+                            if (s2 < wk.S)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) t[q][s2] = __ldcg(base + int64_t(s2) * (BN * 128) + (j0 + q) * 128);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            float v = t[q][0];
+#pragma unroll
+                            for (int s2 = 1; s2 < 16; ++s2)
+                                if (s2 < wk.S) v = __fadd_rn(v, t[q][s2]);
+                            const int64_t m = m0 + j0 + q;
+                            if (col >= 0 && m < p.M) {
+                                if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
+                                store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
+                            }
+                        }
+                    }
                 }
             }
         }
-        cluster_sync_all();  // peers' partial tiles stay alive until every reader is done
     }
 
     if (threadIdx.x == C::kEpiThread0) trace(p, 5);
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) trace(p, 6);
-    if (warp == 1) {
+    if (warp == 1 && !(p.dbg & 16)) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::kTmemCols>(*reinterpret_cast<volatile uint32_t*>(tmem_holder));
     }
@@ -510,59 +512,20 @@ cudaError_t launch_bn_mode(const GemmParams& p, bool pdl, cudaStream_t stream) {
     if (!(configured >> dev & 1)) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
         configured |= uint64_t(1) << dev;
     }
-    if (p.units <= 0) return cudaSuccess;
+    if (p.ctas <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(p.units * p.C));
+    cfg.gridDim = dim3(unsigned(p.ctas));
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    if (pdl) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    if (p.C > 1) {
-        attr[na].id = cudaLaunchAttributeClusterDimension;
-        attr[na].val.clusterDim.x = unsigned(p.C);
-        attr[na].val.clusterDim.y = 1;
-        attr[na].val.clusterDim.z = 1;
-        ++na;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, kern, p);
-}
-
-template <int BN, int MODE>
-int max_clusters_bn_mode(int C) {
-    using Cfg = TcCfg<BN>;
-    auto kern = mixed_gemm_tc_kernel<BN, MODE>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess ||
-        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-        return 0;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(C * 64));
-    cfg.blockDim = dim3(Cfg::kThreads);
-    cfg.dynamicSmemBytes = Cfg::kSmem;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(C);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return n;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 template <int BN>
@@ -584,16 +547,6 @@ int gemm_stages(int bn) {
         case 32: return TcCfg<32>::NS;
         case 64: return TcCfg<64>::NS;
         default: return TcCfg<128>::NS;
-    }
-}
-
-int gemm_max_clusters(int token_tile, int mode, int C) {
-    const bool tok = mode == kFastToken;
-    switch (token_tile) {
-        case 16: return tok ? max_clusters_bn_mode<16, kFastToken>(C) : max_clusters_bn_mode<16, kFastGroup>(C);
-        case 32: return tok ? max_clusters_bn_mode<32, kFastToken>(C) : max_clusters_bn_mode<32, kFastGroup>(C);
-        case 64: return tok ? max_clusters_bn_mode<64, kFastToken>(C) : max_clusters_bn_mode<64, kFastGroup>(C);
-        default: return tok ? max_clusters_bn_mode<128, kFastToken>(C) : max_clusters_bn_mode<128, kFastGroup>(C);
     }
 }
 

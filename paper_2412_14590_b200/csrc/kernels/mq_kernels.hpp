@@ -30,14 +30,15 @@ __host__ __device__ inline uint32_t eal_offset(uint32_t m, uint32_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// K2 schedule. A launch is a grid of UNITS x C CTAs in clusters of C:
-//   C == 1 ("plain"): a unit is one (tile, token block) over all K groups.
-//   C >= 2, even ("paired split-K"): a unit is either ONE sub8 tile split into
-//     C K-slices, or TWO sub4 tiles each split into C/2 K-slices — every CTA
-//     streams about the same bytes (a sub8 group is 2x a sub4 group). The
-//     K-slice partial tiles of an item are reduced in fixed order through
-//     distributed shared memory inside the cluster (deterministic, no global
-//     workspace). Units are ordered token-block-major, sub8 units first.
+// K2 schedule. One CTA per (token block, weight tile, K-slice); a plain grid
+// (no clusters: cluster launches cost several us per kernel at decode sizes).
+// Per token block the CTAs are: S8 slices of every sub8 tile (tile-major),
+// then S4 slices of every sub4 tile. Decode uses S8 = 2*S4 so every CTA
+// streams about the same bytes (a sub8 group is twice a sub4 group). When an
+// item (tile, token block) is split (S > 1), each slice writes its f32 partial
+// tile to its own workspace slot and bumps the item's counter; the LAST slice
+// to arrive sums the S partials in slice order (deterministic) and scatters
+// the result, then re-arms the counter.
 struct GemmParams {
     int32_t T8, T4;         // 128-row tiles of sub8 / sub4
     int64_t n8, n4;         // rows of sub8 / sub4
@@ -57,8 +58,10 @@ struct GemmParams {
     void* Y;
     int32_t out_dtype;      // mq_dtype
     int64_t ldy;
-    int32_t C;              // cluster size (1 = plain)
-    int32_t units;          // grid = units * C
+    int32_t S8, S4;         // K-slices per sub8 / sub4 item
+    int32_t ctas;           // grid size
+    float* part;            // split-K partial tiles [ctas][BN][128] (slot = CTA index)
+    uint32_t* cnt;          // arrival counters [TB * (T8 + T4)], zero between launches
     int32_t rotate;         // 1: each CTA starts its K loop at a CTA-dependent chunk (FAST modes)
     uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int32_t* partials;      // dump mode
@@ -68,28 +71,24 @@ struct GemmParams {
 };
 
 // One CTA's work: rows of `tile` x tokens of block `tb` x groups [g0, g1);
-// the item's S K-slices sit on cluster ranks [rank0, rank0 + S), this CTA is
-// slice `sl`. tile < 0: idle CTA (odd sub4 tile count).
+// slice `sl` of S; the item's slices are CTAs [cta0, cta0 + S).
 struct Work {
-    int tile, tb, g0, g1, S, sl, rank0;
+    int tile, tb, g0, g1, S, sl, cta0, item;
 };
 __host__ __device__ inline Work work_of(const GemmParams& p, int cta) {
     Work w;
-    const int C = p.C;
-    const int unit = cta / C, s = cta - unit * C;
-    const int U1 = C == 1 ? p.T8 + p.T4 : p.T8 + (p.T4 + 1) / 2;  // units per token block
-    w.tb = unit / U1;
-    const int u = unit - w.tb * U1;
-    if (C == 1) {
-        w.tile = u, w.S = 1, w.sl = 0, w.rank0 = 0;
-    } else if (u < p.T8) {
-        w.tile = u, w.S = C, w.sl = s, w.rank0 = 0;
+    const int per_tb = p.S8 * p.T8 + p.S4 * p.T4;
+    w.tb = cta / per_tb;
+    int u = cta - w.tb * per_tb;
+    if (u < p.S8 * p.T8) {
+        w.tile = u / p.S8, w.S = p.S8, w.sl = u - w.tile * p.S8;
     } else {
-        const int half = C / 2;
-        const int t4 = 2 * (u - p.T8) + s / half;
-        w.tile = t4 < p.T4 ? p.T8 + t4 : -1;
-        w.S = half, w.sl = s % half, w.rank0 = (s / half) * half;
+        u -= p.S8 * p.T8;
+        const int t = u / p.S4;
+        w.tile = p.T8 + t, w.S = p.S4, w.sl = u - t * p.S4;
     }
+    w.cta0 = cta - w.sl;
+    w.item = w.tb * (p.T8 + p.T4) + w.tile;
     w.g0 = int((int64_t(w.sl) * p.G) / w.S);
     w.g1 = int((int64_t(w.sl + 1) * p.G) / w.S);
     return w;
@@ -105,8 +104,6 @@ cudaError_t launch_mixed_gemm_tc(const GemmParams& p, int token_tile, int mode, 
 #endif
 constexpr int gemm_gps(int token_tile) { return token_tile <= 32 ? MQ_GPS_SMALL : (token_tile == 64 ? 2 : 1); }
 int gemm_stages(int token_tile);
-// how many clusters of C CTAs of the (FAST-mode) kernel can be co-resident (cudaOccupancyMaxActiveClusters)
-int gemm_max_clusters(int token_tile, int mode, int C);
 // SIMT debug kernel (same weight layout, exact op order, row-major activations).
 cudaError_t launch_mixed_gemm_simt(const GemmParams& p, const int8_t* codes, int64_t ldc,
                                    int mode, int w8_unsigned, cudaStream_t stream);

@@ -10,7 +10,7 @@ reps = 4
 layers = [mq.DeviceLayer(L) for _ in range(reps)]
 dA = torch.from_numpy(A).cuda()
 Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
-opts = mq.exec_opts(capi.MQ_FAST, 128, ksplit=int(os.environ.get("KSPLIT", "0")))
+opts = mq.exec_opts(capi.MQ_FAST, 128, ksplit=int(os.environ.get("KSPLIT", "0")), pdl=os.environ.get("NOPDL", "0") != "1")
 ws = layers[0].quantize_ws(dA, opts)
 for dl in layers: dl.forward_ws(M, ws, out=Y, opts=opts)
 torch.cuda.synchronize()
@@ -21,4 +21,4 @@ g.replay(); torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / 20 * 1e3
-print(f"dbg={os.environ.get('MQ_DBG','0')} ksplit={os.environ.get('KSPLIT','0')} N={N} K={K} M={M}: {us:.2f} us/launch  {layers[0].info.weight_stream_bytes/us/1e3:.0f} GB/s(weights)")
+print(f"dbg={os.environ.get('MQ_DBG','0')} nopdl={os.environ.get('NOPDL','0')} ksplit={os.environ.get('KSPLIT','0')} N={N} K={K} M={M}: {us:.2f} us/launch  {layers[0].info.weight_stream_bytes/us/1e3:.0f} GB/s(weights)")
