@@ -193,27 +193,31 @@ mq_status mq_quantize_act(const void* A, mq_dtype a_dtype, int64_t M, int64_t K,
  * MQ_EXACT: per output element the K-groups run in ascending order with an f32
  *   multiply then an f32 add (gemm.cpp:81), no split-K: bit-identical to the
  *   reference for group-wise activations.
- * MQ_FAST: split-K over groups + FFMA rescale, deterministic fixed-order
- *   split reduction; within the north_star tolerance (<= 1e-3 relative). */
+ * MQ_FAST: FFMA/FFMA2 rescale and, at decode sizes, split-K over groups with a
+ *   deterministic slice-order reduction; within the north_star tolerance
+ *   (<= 1e-3 relative) and bit-reproducible run to run. */
 typedef enum { MQ_EXACT = 0, MQ_FAST = 1 } mq_mode;
 
 typedef struct {
     int32_t mode;        /* mq_mode */
     int32_t act_group;   /* group size the activation scales use (g or K) */
-    int32_t ksplit;      /* 0 = auto stream-K (MQ_FAST); 1 = no K splitting */
+    int32_t ksplit;      /* MQ_FAST: 0 = auto, 1 = no K splitting, 2..8 = K-slices per sub4 tile */
     int32_t token_tile;  /* 0 = auto; else 16/32/64/128 */
     int32_t gemm_impl;   /* 0 = tcgen05 (product); 1 = SIMT debug kernel */
     int32_t no_pdl;      /* 1 = plain launches (default: programmatic dependent launch) */
 } mq_exec_opts;
 
-/* Bytes of scratch a forward needs (split-K partials + counters). */
+/* Bytes of scratch a forward needs: split-K arrival counters + partial tiles
+ * and the engine-layout activations (K1 output, or the repacked codes). */
 size_t mq_forward_workspace_bytes(mq_layer_t layer, int64_t M, const mq_exec_opts* opts);
 
 /* The mixed-precision linear on quantized activations
  * (execute_mixed_on_codes, gemm.cpp:140-181): both sub-problems in one
- * persistent launch, scatter fused into the epilogue.
- * codes: device int8 [M, ldc] (16-byte aligned, ldc % 16 == 0); scales as
- * mq_quantize_act wrote them (group-major, lds % 4 == 0, 16-byte aligned);
+ * persistent launch, scatter fused into the epilogue. The codes are first
+ * repacked into the engine activation layout (one small kernel);
+ * mq_mixed_linear / mq_quantize_act_ws write that layout directly.
+ * codes: device int8 [M, ldc] (ldc >= K); scales as mq_quantize_act wrote them
+ * (group-major [G, lds], lds >= M; per-token: [M]);
  * Y: device [M, out_features] row-major in out_dtype (sharded layers: the
  * rank's [M, shard_cols] block in gather order).
  * workspace: device, >= mq_forward_workspace_bytes, zero-initialised once

@@ -64,27 +64,35 @@ int auto_token_tile(int64_t M) {
 }
 
 struct Plan {
-    int bn, tb, mode, per_token, S4, S8, ctas;
+    int bn, tb, mode, per_token, S4, S8, units, grid;
     int64_t Mpad;
     bool pdl, rotate;
 };
 
 // K-slices per item (mq_kernels.hpp schedule). Exact mode keeps the
 // reference's ascending group order per output, so it never splits; token-
-// tiled (prefill) launches are tensor-bound and use one tile per CTA. Decode
-// splits sub4 tiles S ways and sub8 tiles 2S ways (equal bytes per CTA), S as
-// large as one wave of SMs allows.
+// tiled (prefill) launches are tensor-bound and use one tile per unit. Decode
+// splits sub4 tiles S ways and sub8 tiles 2S ways (equal bytes per unit).
 void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
     pl->S4 = pl->S8 = 1;
-    if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1) return;
-    int S = ksplit >= 2 ? ksplit : 1;
-    if (ksplit == 0) {
-        const int64_t base = 2 * L->tiles8 + L->tiles4;
-        S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, L->num_sms / std::max<int64_t>(base, 1))));
+    if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1 || pl->bn > 32) return;
+    int best = 1;
+    if (ksplit >= 2) {
+        best = ksplit;
+    } else {
+        // the largest S whose units still fit one round of the persistent grid
+        // (a split reduction on the critical path of a multi-round CTA costs more
+        // than the balance it buys)
+        for (int S = 2; S <= 8; ++S) {
+            if (L->G / S < 2) break;
+            if (2 * S * L->tiles8 + S * L->tiles4 <= L->num_sms) best = S;
+        }
     }
-    S = std::max(1, std::min(S, L->G / 2));
-    pl->S4 = S;
-    pl->S8 = std::min(2 * S, std::max(1, L->G));
+    pl->S4 = best;
+    // sub8 tiles stream twice the bytes of sub4 tiles: halve them too while
+    // everything still fits one round
+    const bool halve8 = best > 1 || 2 * L->tiles8 + L->tiles4 <= L->num_sms;
+    pl->S8 = halve8 ? std::min(2 * best, std::max(1, L->G)) : 1;
 }
 
 mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
@@ -108,7 +116,8 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     pl->pdl = o->no_pdl == 0;
     pl->rotate = o->mode == MQ_FAST;
     choose_split(L, pl, o->ksplit);
-    pl->ctas = static_cast<int>((int64_t(pl->S8) * L->tiles8 + int64_t(pl->S4) * L->tiles4) * pl->tb);
+    pl->units = static_cast<int>((int64_t(pl->S8) * L->tiles8 + int64_t(pl->S4) * L->tiles4) * pl->tb);
+    pl->grid = std::min(pl->units, L->num_sms);
     return MQ_OK;
 }
 
@@ -124,7 +133,7 @@ EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
     const size_t items = size_t(pl.tb) * size_t(L->tiles8 + L->tiles4);
     w.off_part = al(items * 4);
     const bool split = pl.S4 > 1 || pl.S8 > 1;
-    w.off_acts = w.off_part + (split ? al(size_t(pl.ctas) * 128 * size_t(pl.bn) * 4) : 0);
+    w.off_acts = w.off_part + (split ? al(size_t(pl.units) * 128 * size_t(pl.bn) * 4) : 0);
     w.off_sa = w.off_acts + al(size_t(L->G) * size_t(pl.Mpad) * 128);
     const int64_t Ga = pl.per_token ? 1 : L->G;
     w.total = w.off_sa + al(size_t(Ga) * size_t(pl.Mpad) * 4);
@@ -149,7 +158,8 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dty
     p->ldy = L->world > 1 ? L->shard_cols : L->N;
     p->S4 = pl.S4;
     p->S8 = pl.S8;
-    p->ctas = pl.ctas;
+    p->units = pl.units;
+    p->grid = pl.grid;
     p->rotate = pl.rotate ? 1 : 0;
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
     static const int dbg = [] {
@@ -509,7 +519,8 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
     }
     if (p.T8 + p.T4 == 0) return MQ_OK;
     p.S4 = p.S8 = 1;
-    p.ctas = (p.T8 + p.T4) * pl.tb;
+    p.units = (p.T8 + p.T4) * pl.tb;
+    p.grid = std::min(p.units, L->num_sms);
     p.partials = partials;
     p.partial_rows = static_cast<int32_t>(which == 0 ? L->n8 : L->n4);
     e = launch_mixed_gemm_tc(p, pl.bn, kDumpPartials, false, s);

@@ -53,8 +53,8 @@ __global__ void act_quant_group_kernel(const void* __restrict__ A, int64_t M, in
                                        int64_t lda, int group, int G, int f16,
                                        int8_t* __restrict__ codes, int64_t ldc,
                                        float* __restrict__ scales, int64_t lds, int32_t* err) {
-    griddep_wait();
-    griddep_launch();
+    griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
+    griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= M * G) return;
@@ -88,8 +88,8 @@ template <int DT>
 __global__ void __launch_bounds__(256) act_quant_row_kernel(
     const void* __restrict__ A, int64_t K, int64_t lda, int f16, int8_t* __restrict__ codes,
     int64_t ldc, float* __restrict__ scales, int32_t* err) {
-    griddep_wait();
-    griddep_launch();
+    griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
+    griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     __shared__ float red[8];
     __shared__ int bad[8];
     const int64_t m = blockIdx.x;
@@ -132,8 +132,8 @@ template <int DT>
 __global__ void act_quant_eal_group_kernel(const void* __restrict__ A, int64_t M, int64_t K, int64_t lda, int G,
                                            int64_t Mpad, uint8_t* __restrict__ acts, float* __restrict__ sa,
                                            int32_t* err) {
-    griddep_wait();
-    griddep_launch();
+    griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
+    griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= Mpad * G) return;
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(256) act_quant_eal_row_kernel(const void* __re
                                                                 int64_t lda, int G, int64_t Mpad,
                                                                 uint8_t* __restrict__ acts, float* __restrict__ sa,
                                                                 int32_t* err) {
-    griddep_wait();
-    griddep_launch();
+    griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
+    griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     __shared__ float red[8];
     __shared__ int bad[8];
     const int64_t m = blockIdx.x;

@@ -130,6 +130,26 @@ struct Ring {
     }
 };
 
+// f32x2 (FFMA2 / FMUL2 on sm_100): two f32 lanes in one 64-bit register pair.
+// FAST modes only — ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2, so
+// the exact (reference op order) mode stays scalar.
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
 // nibbles of one packed word -> two words of int8 (c - z): codes 0..3 and 4..7
 __device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& lo, uint32_t& hi) {
     lo = ((w & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
@@ -183,20 +203,33 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     if (threadIdx.x == 0) trace(p, 0);
     griddep_launch();  // let the next kernel in the stream start its prologue
 
-    const Work wk = work_of(p, blockIdx.x);
-    const bool live = true;
-    const TileInfo ti = tile_info(p, live ? wk.tile : 0);
-    const int gps = ti.is8 ? C::GPS8 : GPS;
-    const int nch = (live && !(p.dbg & 8)) ? (wk.g1 - wk.g0 + gps - 1) / gps : 0;  // dbg&8: launch-floor probe
-    // FAST modes start each CTA at a different chunk of its K-slice so the CTAs
-    // of a launch do not all read the same activation lines at the same time
-    const int rot = (p.rotate && nch > 1) ? int((blockIdx.x * 7u) % uint32_t(nch)) : 0;
-    auto chunk_at = [&](int i, int& gc, int& cg) {
-        int c = i + rot;
-        if (c >= nch) c -= nch;
-        gc = wk.g0 + c * gps;
-        cg = (wk.g1 - gc) < gps ? (wk.g1 - gc) : gps;
+    // Persistent: CTA b walks work units b, b + grid, b + 2 grid, ... (each unit
+    // = one (tile, token block, K-slice), mq_kernels.hpp); every role walks the
+    // same (unit, chunk) sequence, so the rings run on across units and the next
+    // unit's weights stream while the current unit's epilogue finishes.
+    struct Unit {
+        Work wk;
+        TileInfo ti;
+        int gps, nch, rot;
     };
+    auto unit_at = [&](int u) {
+        Unit U;
+        U.wk = work_of(p, u);
+        U.ti = tile_info(p, U.wk.tile);
+        U.gps = U.ti.is8 ? C::GPS8 : GPS;
+        U.nch = (p.dbg & 8) ? 0 : (U.wk.g1 - U.wk.g0 + U.gps - 1) / U.gps;  // dbg&8: launch-floor probe
+        // FAST modes start each unit at a different chunk of its K-slice so the
+        // CTAs do not all read the same activation lines at the same time
+        U.rot = (p.rotate && U.nch > 1) ? int((uint32_t(u) * 7u) % uint32_t(U.nch)) : 0;
+        return U;
+    };
+    auto chunk_at = [&](const Unit& U, int i, int& gc, int& cg) {
+        int c = i + U.rot;
+        if (c >= U.nch) c -= U.nch;
+        gc = U.wk.g0 + c * U.gps;
+        cg = (U.wk.g1 - gc) < U.gps ? (U.wk.g1 - gc) : U.gps;
+    };
+    const int u0 = blockIdx.x, ustep = gridDim.x;
 
     if (warp == 0) {
         // ============================== producer ==============================
@@ -212,45 +245,51 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 if (lane == 0) trace(p, 2);
             }
             Ring rr;
-            for (int n = 0; n < nch; ++n) {
-                const bool pre = n < NS;
-                if (pass == 0 && !pre) break;
-                int gc, cg;
-                chunk_at(n, gc, cg);
-                uint8_t* st = stage(rr.idx);
-                if (pass == 0 || !pre) {
-                    if (pass == 1) ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
-                    if (lane == 0) trace_chunk(p, 0, n);
-                    const uint32_t wbytes = uint32_t(cg * ti.blk);
-                    const uint32_t abytes = uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0));
-                    if (elect_one()) {
-                        ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes + abytes);
-                        ptx::bulk_g2s(st, p.wq + ti.off + int64_t(gc) * ti.blk, wbytes, &full[rr.idx], pol_w);
+            int n = 0;  // chunk counter across units
+            for (int u = u0; u < p.units; u += ustep) {
+                const Unit U = unit_at(u);
+                if (pass == 0 && n >= NS) break;
+                for (int i = 0; i < U.nch; ++i, ++n) {
+                    const bool pre = n < NS;
+                    if (pass == 0 && !pre) break;
+                    int gc, cg;
+                    chunk_at(U, i, gc, cg);
+                    uint8_t* st = stage(rr.idx);
+                    if (pass == 0 || !pre) {
+                        if (pass == 1) ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
+                        if (lane == 0) trace_chunk(p, 0, n);
+                        const uint32_t wbytes = uint32_t(cg * U.ti.blk);
+                        const uint32_t abytes = uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0));
+                        if (elect_one()) {
+                            ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes + abytes);
+                            ptx::bulk_g2s(st, p.wq + U.ti.off + int64_t(gc) * U.ti.blk, wbytes, &full[rr.idx], pol_w);
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
-                }
-                if (pass == 1) {
-                    if (elect_one()) {
-                        const int64_t row0 = int64_t(wk.tb) * BN;
-                        if (contig) {
-                            ptx::bulk_g2s(st + C::kOffB, p.acts + int64_t(gc) * p.Mpad * 128, uint32_t(cg * BN * 128),
-                                          &full[rr.idx], pol_a);
-                            if (kSa)
-                                ptx::bulk_g2s(st + C::kOffSa, p.sa + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4),
+                    if (pass == 1) {
+                        if (elect_one()) {
+                            const int64_t row0 = int64_t(U.wk.tb) * BN;
+                            if (contig) {
+                                ptx::bulk_g2s(st + C::kOffB, p.acts + int64_t(gc) * p.Mpad * 128, uint32_t(cg * BN * 128),
                                               &full[rr.idx], pol_a);
-                        } else {
-                            for (int j = 0; j < cg; ++j) {
-                                ptx::bulk_g2s(st + C::kOffB + j * BN * 128, p.acts + (int64_t(gc + j) * p.Mpad + row0) * 128,
-                                              uint32_t(BN * 128), &full[rr.idx], pol_a);
                                 if (kSa)
-                                    ptx::bulk_g2s(st + C::kOffSa + j * BN * 4, p.sa + int64_t(gc + j) * p.Mpad + row0,
-                                                  uint32_t(BN * 4), &full[rr.idx], pol_a);
+                                    ptx::bulk_g2s(st + C::kOffSa, p.sa + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4),
+                                                  &full[rr.idx], pol_a);
+                            } else {
+                                for (int j = 0; j < cg; ++j) {
+                                    ptx::bulk_g2s(st + C::kOffB + j * BN * 128,
+                                                  p.acts + (int64_t(gc + j) * p.Mpad + row0) * 128, uint32_t(BN * 128),
+                                                  &full[rr.idx], pol_a);
+                                    if (kSa)
+                                        ptx::bulk_g2s(st + C::kOffSa + j * BN * 4, p.sa + int64_t(gc + j) * p.Mpad + row0,
+                                                      uint32_t(BN * 4), &full[rr.idx], pol_a);
+                                }
                             }
                         }
+                        __syncwarp();
                     }
-                    __syncwarp();
+                    rr.next<NS>();
                 }
-                rr.next<NS>();
             }
         }
     } else if (warp == 1) {
@@ -264,44 +303,48 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         const uint32_t idesc4 = idesc_i8(BN, true, true);
         const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
         Ring rs, ra, rt;
-        for (int n = 0; n < nch; ++n) {
-            int gc, cg;
-            chunk_at(n, gc, cg);
-            ptx::mbar_wait(&full[rs.idx], rs.ph);
-            ptx::mbar_wait(&afull[ra.idx], ra.ph);
-            ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
-            ptx::tc_fence_after();
-            if (lane == 0) trace_chunk(p, 1, n);
-            const uint32_t st = ptx::smem_u32(stage(rs.idx));
-            if (elect_one()) {
-                if (!(p.dbg & 4)) {
-                    for (int j = 0; j < cg; ++j) {
-                        const uint32_t d_tmem = tmem_base + uint32_t((rt.idx * GPS + j) * BN);
-                        const uint32_t b_addr = st + C::kOffB + j * (BN * 128);
-                        if (ti.is8) {
-                            const uint32_t a_addr = st + j * kBlock8Bytes;
+        int n = 0;
+        for (int u = u0; u < p.units; u += ustep) {
+            const Unit U = unit_at(u);
+            for (int i = 0; i < U.nch; ++i, ++n) {
+                int gc, cg;
+                chunk_at(U, i, gc, cg);
+                ptx::mbar_wait(&full[rs.idx], rs.ph);
+                ptx::mbar_wait(&afull[ra.idx], ra.ph);
+                ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
+                ptx::tc_fence_after();
+                if (lane == 0) trace_chunk(p, 1, n);
+                const uint32_t st = ptx::smem_u32(stage(rs.idx));
+                if (elect_one()) {
+                    if (!(p.dbg & 4)) {
+                        for (int j = 0; j < cg; ++j) {
+                            const uint32_t d_tmem = tmem_base + uint32_t((rt.idx * GPS + j) * BN);
+                            const uint32_t b_addr = st + C::kOffB + j * (BN * 128);
+                            if (U.ti.is8) {
+                                const uint32_t a_addr = st + j * kBlock8Bytes;
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                ptx::mma_i8_ss(d_tmem, ptx::umma_desc_sw128(a_addr + 32 * k),
-                                               ptx::umma_desc_sw128(b_addr + 32 * k), idesc8, k > 0);
-                        } else {
-                            const uint32_t a_tmem = tmem_base + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32);
+                                for (int k = 0; k < 4; ++k)
+                                    ptx::mma_i8_ss(d_tmem, ptx::umma_desc_sw128(a_addr + 32 * k),
+                                                   ptx::umma_desc_sw128(b_addr + 32 * k), idesc8, k > 0);
+                            } else {
+                                const uint32_t a_tmem = tmem_base + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32);
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                ptx::mma_i8_ts(d_tmem, a_tmem + 8 * k, ptx::umma_desc_sw128(b_addr + 32 * k), idesc4,
-                                               k > 0);
+                                for (int k = 0; k < 4; ++k)
+                                    ptx::mma_i8_ts(d_tmem, a_tmem + 8 * k, ptx::umma_desc_sw128(b_addr + 32 * k), idesc4,
+                                                   k > 0);
+                            }
                         }
                     }
+                    ptx::tc_commit(&tfull[rt.idx]);
+                    ptx::tc_commit(&aempty[ra.idx]);
+                    ptx::tc_commit(&empty[rs.idx]);
                 }
-                ptx::tc_commit(&tfull[rt.idx]);
-                ptx::tc_commit(&aempty[ra.idx]);
-                ptx::tc_commit(&empty[rs.idx]);
+                __syncwarp();
+                if (lane == 0) trace_chunk(p, 2, n);
+                ra.next<NA>();
+                rt.next<NT>();
+                rs.next<NS>();
             }
-            __syncwarp();
-            if (lane == 0) trace_chunk(p, 2, n);
-            ra.next<NA>();
-            rt.next<NT>();
-            rs.next<NS>();
         }
     } else if (warp >= 4 && warp < 4 + 4 * NC) {
         // ============ converter (sub4 -> int8 A tiles in TMEM; scales -> meta ring) ============
@@ -311,130 +354,192 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         ptx::tc_fence_after();
         const uint32_t tmem_row = *reinterpret_cast<volatile uint32_t*>(tmem_holder) + (uint32_t((warp & 3) * 32) << 16);
         Ring rs, ra, rt;
-        for (int n = 0; n < nch; ++n) {
-            int gc, cg;
-            chunk_at(n, gc, cg);
-            // every chunk (sub8 too): wait for the stage, a free A slot and a free
-            // meta slot (a role that skipped chunks could run two phases ahead of
-            // a barrier and read an older phase's parity as complete)
-            ptx::mbar_wait(&full[rs.idx], rs.ph);
-            if (threadIdx.x == 128) trace_chunk(p, 5, n);
-            ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
-            ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
-            if (threadIdx.x == 128) trace_chunk(p, 6, n);
-            const uint8_t* st = stage(rs.idx);
-            float* msw = meta + rt.idx * (C::kMetaSlot / 4);
-            for (int j = wg; j < cg; j += NC) {
-                if (!ti.is8) {
-                    const uint8_t* raw = st + j * kBlock4Bytes;
-                    const uint32_t kk = uint32_t(128 - raw[kCodes4Bytes + 512 + r]) * 0x01010101u;
-                    uint32_t v[32];
+        int n = 0;
+        for (int u = u0; u < p.units; u += ustep) {
+            const Unit U = unit_at(u);
+            for (int i = 0; i < U.nch; ++i, ++n) {
+                int gc, cg;
+                chunk_at(U, i, gc, cg);
+                // every chunk (sub8 too): wait for the stage, a free A slot and a free
+                // meta slot (a role that skipped chunks could run two phases ahead of
+                // a barrier and read an older phase's parity as complete)
+                ptx::mbar_wait(&full[rs.idx], rs.ph);
+                if (threadIdx.x == 128) trace_chunk(p, 5, n);
+                ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
+                ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
+                if (threadIdx.x == 128) trace_chunk(p, 6, n);
+                const uint8_t* st = stage(rs.idx);
+                float* msw = meta + rt.idx * (C::kMetaSlot / 4);
+                for (int j = wg; j < cg; j += NC) {
+                    if (!U.ti.is8) {
+                        const uint8_t* raw = st + j * kBlock4Bytes;
+                        const uint32_t kk = uint32_t(128 - raw[kCodes4Bytes + 512 + r]) * 0x01010101u;
+                        uint32_t v[32];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint4 w = *reinterpret_cast<const uint4*>(raw + q * 2048 + r * 16);
-                        unpack_word(w.x, kk, v[q * 8 + 0], v[q * 8 + 1]);
-                        unpack_word(w.y, kk, v[q * 8 + 2], v[q * 8 + 3]);
-                        unpack_word(w.z, kk, v[q * 8 + 4], v[q * 8 + 5]);
-                        unpack_word(w.w, kk, v[q * 8 + 6], v[q * 8 + 7]);
+                        for (int q = 0; q < 4; ++q) {
+                            const uint4 w = *reinterpret_cast<const uint4*>(raw + q * 2048 + r * 16);
+                            unpack_word(w.x, kk, v[q * 8 + 0], v[q * 8 + 1]);
+                            unpack_word(w.y, kk, v[q * 8 + 2], v[q * 8 + 3]);
+                            unpack_word(w.z, kk, v[q * 8 + 4], v[q * 8 + 5]);
+                            unpack_word(w.w, kk, v[q * 8 + 6], v[q * 8 + 7]);
+                        }
+                        if (!(p.dbg & 2)) ptx::tmem_st32(tmem_row + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32), v);
+                        msw[j * 128 + r] = reinterpret_cast<const float*>(raw + kCodes4Bytes)[r];
+                    } else {
+                        msw[j * 128 + r] = reinterpret_cast<const float*>(st + j * kBlock8Bytes + kCodes8Bytes)[r];
                     }
-                    if (!(p.dbg & 2)) ptx::tmem_st32(tmem_row + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32), v);
-                    msw[j * 128 + r] = reinterpret_cast<const float*>(raw + kCodes4Bytes)[r];
-                } else {
-                    msw[j * 128 + r] = reinterpret_cast<const float*>(st + j * kBlock8Bytes + kCodes8Bytes)[r];
                 }
+                if (kSa && wg == 0 && r < cg * BN) msw[GPS * 128 + r] = reinterpret_cast<const float*>(st + C::kOffSa)[r];
+                if (!U.ti.is8) ptx::tmem_wait_st();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&mfull[rt.idx]);
+                    ptx::mbar_arrive(&afull[ra.idx]);
+                    ptx::mbar_arrive(&empty[rs.idx]);
+                }
+                if (threadIdx.x == 128) trace_chunk(p, 3, n);
+                ra.next<NA>();
+                rt.next<NT>();
+                rs.next<NS>();
             }
-            if (kSa && wg == 0 && r < cg * BN) msw[GPS * 128 + r] = reinterpret_cast<const float*>(st + C::kOffSa)[r];
-            if (!ti.is8) ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                ptx::mbar_arrive(&mfull[rt.idx]);
-                ptx::mbar_arrive(&afull[ra.idx]);
-                ptx::mbar_arrive(&empty[rs.idx]);
-            }
-            if (threadIdx.x == 128) trace_chunk(p, 3, n);
-            ra.next<NA>();
-            rt.next<NT>();
-            rs.next<NS>();
         }
-    }
-
-    // ================================ epilogue ================================
-    const bool is_epi = int(threadIdx.x) >= C::kEpiThread0;
-    const int et = threadIdx.x - C::kEpiThread0;  // 0 .. 128*NE-1
-    const int e = et >> 7;                        // epilogue warpgroup
-    const int wq = warp & 3;                      // TMEM lane quarter this warp may access
-    const int r = wq * 32 + lane;                 // tile row (= TMEM lane)
-    const int c0 = e * BNE;                       // first token column of this warpgroup
-    const int64_t m0 = int64_t(wk.tb) * BN + c0;  // first token of this warpgroup
-    if (is_epi) {
-        float acc[BNE];
-#pragma unroll
-        for (int j = 0; j < BNE; ++j) acc[j] = 0.0f;
-        float sat[MODE == kExactToken ? BNE : 1];  // per-token s_a of this warpgroup's tokens
+    } else if (int(threadIdx.x) >= C::kEpiThread0) {
+        // ================================ epilogue ================================
+        const int et = threadIdx.x - C::kEpiThread0;  // 0 .. 128*NE-1
+        const int e = et >> 7;                        // epilogue warpgroup
+        const int wq = warp & 3;                      // TMEM lane quarter this warp may access
+        const int r = wq * 32 + lane;                 // tile row (= TMEM lane)
+        const int c0 = e * BNE;                       // first token column of this warpgroup
         ptx::mbar_wait(tmem_ready, 0);
         ptx::tc_fence_after();
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
         griddep_wait();  // scales / output of this launch are ours now
-        if constexpr (MODE == kExactToken) {
-#pragma unroll
-            for (int j = 0; j < BNE; ++j) sat[j] = m0 + j < p.M ? __ldg(p.sa + m0 + j) : 0.0f;
-        }
         Ring rt;
-        for (int n = 0; n < nch; ++n) {
-            int gc, cg;
-            chunk_at(n, gc, cg);
-            ptx::mbar_wait(&mfull[rt.idx], rt.ph);
-            ptx::mbar_wait(&tfull[rt.idx], rt.ph);
-            ptx::tc_fence_after();
-            if (n == 0 && et == 0) trace(p, 3);
-            const float* msw = meta + rt.idx * (C::kMetaSlot / 4);
-            for (int j = 0; j < cg; ++j) {
-                const float sw = msw[j * 128 + r];
-                const float* sav = msw + GPS * 128 + j * BN + c0;
-                const uint32_t tcol = uint32_t((rt.idx * GPS + j) * BN + c0);
+        int n = 0;
+        for (int u = u0; u < p.units; u += ustep) {
+            const Unit U = unit_at(u);
+            const Work& wk = U.wk;
+            const TileInfo& ti = U.ti;
+            const int64_t m0 = int64_t(wk.tb) * BN + c0;  // first token of this warpgroup
+            constexpr bool kPair = (MODE == kFastGroup || MODE == kFastToken);
+            float acc[BNE];
+            uint64_t acc2[kPair ? BNE / 2 : 1];  // FAST modes accumulate in f32x2 pairs
+            if constexpr (kPair) {
 #pragma unroll
-                for (int ch = 0; ch < BNE / 16; ++ch) {
-                    if (p.dbg & 1) break;
-                    uint32_t v[16];
-                    ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * 16, v);
-                    ptx::tmem_wait_ld();
-                    if constexpr (MODE == kDumpPartials) {
-                        if (r < ti.rows) {
+                for (int j = 0; j < BNE / 2; ++j) acc2[j] = 0ull;
+            } else {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) {
-                                const int64_t m = m0 + ch * 16 + i;
-                                if (m < p.M)
-                                    p.partials[(int64_t(gc + j) * p.M + m) * p.partial_rows + ti.first + r] = int32_t(v[i]);
+                for (int j = 0; j < BNE; ++j) acc[j] = 0.0f;
+            }
+            float sat[MODE == kExactToken ? BNE : 1];  // per-token s_a of this warpgroup's tokens
+            if constexpr (MODE == kExactToken) {
+#pragma unroll
+                for (int j = 0; j < BNE; ++j) sat[j] = m0 + j < p.M ? __ldg(p.sa + m0 + j) : 0.0f;
+            }
+            for (int i = 0; i < U.nch; ++i, ++n) {
+                int gc, cg;
+                chunk_at(U, i, gc, cg);
+                ptx::mbar_wait(&mfull[rt.idx], rt.ph);
+                ptx::mbar_wait(&tfull[rt.idx], rt.ph);
+                ptx::tc_fence_after();
+                if (n == 0 && et == 0) trace(p, 3);
+                const float* msw = meta + rt.idx * (C::kMetaSlot / 4);
+                if constexpr (kPair && BNE == 16) {
+                    // decode: two groups' sums in flight per wait (register budget at 512 threads)
+#pragma unroll
+                    for (int j0 = 0; j0 < GPS; j0 += 2) {
+                        if (j0 >= cg || (p.dbg & 1)) break;
+                        uint32_t v[2][16];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            if (j0 + h < cg)
+                                ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + uint32_t((rt.idx * GPS + j0 + h) * BN + c0),
+                                               v[h]);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (j0 + h >= cg) break;
+                            const int j = j0 + h;
+                            const float sw = msw[j * 128 + r];
+                            const uint64_t sw2 = pk2(sw, sw);
+                            const float* sav = msw + GPS * 128 + j * BN + c0;
+#pragma unroll
+                            for (int q = 0; q < 16; q += 2) {
+                                const uint64_t g2 = pk2(__int2float_rn(int32_t(v[h][q])), __int2float_rn(int32_t(v[h][q + 1])));
+                                if constexpr (MODE == kFastGroup)
+                                    acc2[q / 2] = fma2(g2, mul2(*reinterpret_cast<const uint64_t*>(sav + q), sw2), acc2[q / 2]);
+                                else
+                                    acc2[q / 2] = fma2(g2, sw2, acc2[q / 2]);
                             }
                         }
-                    } else {
+                    }
+                } else
+                for (int j = 0; j < cg; ++j) {
+                    const float sw = msw[j * 128 + r];
+                    const float* sav = msw + GPS * 128 + j * BN + c0;
+                    const uint64_t sw2 = pk2(sw, sw);
+                    const uint32_t tcol = uint32_t((rt.idx * GPS + j) * BN + c0);
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float gs = __int2float_rn(int32_t(v[i]));  // exact: |S| < 2^22
-                            const int jj = ch * 16 + i;
-                            if constexpr (MODE == kExactGroup) {
-                                // gemm.cpp:81 — out += gs * (s_a * s_w), no contraction
-                                acc[jj] = __fadd_rn(acc[jj], __fmul_rn(gs, __fmul_rn(sav[jj], sw)));
-                            } else if constexpr (MODE == kExactToken) {
-                                acc[jj] = __fadd_rn(acc[jj], __fmul_rn(gs, __fmul_rn(sat[jj], sw)));
-                            } else if constexpr (MODE == kFastGroup) {
-                                acc[jj] = __fmaf_rn(gs, __fmul_rn(sav[jj], sw), acc[jj]);
-                            } else {
-                                acc[jj] = __fmaf_rn(gs, sw, acc[jj]);
+                    for (int ch = 0; ch < BNE / 16; ++ch) {
+                        if (p.dbg & 1) break;
+                        uint32_t v[16];
+                        ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * 16, v);
+                        ptx::tmem_wait_ld();
+                        if constexpr (MODE == kDumpPartials) {
+                            if (r < ti.rows) {
+#pragma unroll
+                                for (int q = 0; q < 16; ++q) {
+                                    const int64_t m = m0 + ch * 16 + q;
+                                    if (m < p.M)
+                                        p.partials[(int64_t(gc + j) * p.M + m) * p.partial_rows + ti.first + r] =
+                                            int32_t(v[q]);
+                                }
+                            }
+                        } else if constexpr (kPair) {
+#pragma unroll
+                            for (int q = 0; q < 16; q += 2) {
+                                const int jj = ch * 16 + q;
+                                // exact int -> f32 (|S| < 2^22), two lanes per FFMA2
+                                const uint64_t g2 = pk2(__int2float_rn(int32_t(v[q])), __int2float_rn(int32_t(v[q + 1])));
+                                if constexpr (MODE == kFastGroup) {
+                                    const uint64_t sa2 = *reinterpret_cast<const uint64_t*>(sav + jj);
+                                    acc2[jj / 2] = fma2(g2, mul2(sa2, sw2), acc2[jj / 2]);
+                                } else {
+                                    acc2[jj / 2] = fma2(g2, sw2, acc2[jj / 2]);
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) {
+                                const float gs = __int2float_rn(int32_t(v[q]));  // exact: |S| < 2^22
+                                const int jj = ch * 16 + q;
+                                if constexpr (MODE == kExactGroup) {
+                                    // gemm.cpp:81 — out += gs * (s_a * s_w), no contraction
+                                    acc[jj] = __fadd_rn(acc[jj], __fmul_rn(gs, __fmul_rn(sav[jj], sw)));
+                                } else if constexpr (MODE == kExactToken) {
+                                    acc[jj] = __fadd_rn(acc[jj], __fmul_rn(gs, __fmul_rn(sat[jj], sw)));
+                                } else if constexpr (MODE == kFastGroup) {
+                                    acc[jj] = __fmaf_rn(gs, __fmul_rn(sav[jj], sw), acc[jj]);
+                                } else {
+                                    acc[jj] = __fmaf_rn(gs, sw, acc[jj]);
+                                }
                             }
                         }
                     }
                 }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[rt.idx]);
+                if (et == 0) trace_chunk(p, 4, n);
+                rt.next<NT>();
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[rt.idx]);
-            if (et == 0) trace_chunk(p, 4, n);
-            rt.next<NT>();
-        }
-        if (et == 0) trace(p, 4);
-        if (MODE != kDumpPartials && live) {
+            if (et == 0) trace(p, 4);
+            if constexpr (kPair) {
+#pragma unroll
+                for (int j = 0; j < BNE / 2; ++j) upk2(acc2[j], acc[2 * j], acc[2 * j + 1]);
+            }
+            if (MODE == kDumpPartials || U.nch == 0) continue;
             if (wk.S == 1) {
                 // whole-K tile: scatter straight to the original output columns
                 const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
@@ -449,46 +554,51 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                         }
                     }
                 }
-            } else {
-                // split-K: publish this slice's partial tile, count arrivals; the
-                // last slice sums all S partials in slice order and scatters them
-                float* mine = p.part + int64_t(blockIdx.x) * (BN * 128);
+                continue;
+            }
+            // split-K (decode token tiles only): publish this slice's partial tile
+            // [BN][128] (slot = unit), count arrivals; the last slice sums all S
+            // partials in slice order (deterministic) and scatters them
+            if constexpr (BN <= 32) {
+            float* mine = p.part + int64_t(u) * (BN * 128);
 #pragma unroll
-                for (int j = 0; j < BNE; ++j) __stcg(mine + (c0 + j) * 128 + r, acc[j]);
-                named_bar_sync(2, 128 * NE);
-                if (et == 0) {
-                    __threadfence();
-                    const uint32_t prev = atomicAdd(p.cnt + wk.item, 1u);
-                    *s_last = prev == uint32_t(wk.S - 1);
-                    if (prev == uint32_t(wk.S - 1)) p.cnt[wk.item] = 0u;  // re-arm for the next launch
-                }
-                named_bar_sync(2, 128 * NE);
-                if (*s_last) {
-                    __threadfence();
-                    const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
-                    const float* base = p.part + int64_t(wk.cta0) * (BN * 128) + c0 * 128 + r;
-                    for (int j0 = 0; j0 < BNE; j0 += 4) {
-                        float t[4][16];
+            for (int j = 0; j < BNE; ++j) __stcg(mine + (c0 + j) * 128 + r, acc[j]);
+            named_bar_sync(2, 128 * NE);
+            if (et == 0) {
+                __threadfence();
+                const uint32_t prev = atomicAdd(p.cnt + wk.item, 1u);
+                *s_last = prev == uint32_t(wk.S - 1);
+                if (prev == uint32_t(wk.S - 1)) p.cnt[wk.item] = 0u;  // re-arm for the next launch
+            }
+            named_bar_sync(2, 128 * NE);
+            const bool last = *s_last != 0;
+            named_bar_sync(2, 128 * NE);  // s_last is reused by the next unit
+            if (last) {
+                __threadfence();
+                const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
+                const float* base = p.part + int64_t(wk.cta0) * (BN * 128) + c0 * 128 + r;
+                for (int j0 = 0; j0 < BNE; j0 += 2) {
+                    float t[2][16];
 #pragma unroll
-                        for (int s2 = 0; s2 < 16; ++s2)
-                            if (s2 < wk.S)
+                    for (int s2 = 0; s2 < 16; ++s2)
+                        if (s2 < wk.S)
 #pragma unroll
-                                for (int q = 0; q < 4; ++q) t[q][s2] = __ldcg(base + int64_t(s2) * (BN * 128) + (j0 + q) * 128);
+                            for (int q = 0; q < 2; ++q) t[q][s2] = __ldcg(base + int64_t(s2) * (BN * 128) + (j0 + q) * 128);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            float v = t[q][0];
+                    for (int q = 0; q < 2; ++q) {
+                        float v = t[q][0];
 #pragma unroll
-                            for (int s2 = 1; s2 < 16; ++s2)
-                                if (s2 < wk.S) v = __fadd_rn(v, t[q][s2]);
-                            const int64_t m = m0 + j0 + q;
-                            if (col >= 0 && m < p.M) {
-                                if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                                store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
-                            }
+                        for (int s2 = 1; s2 < 16; ++s2)
+                            if (s2 < wk.S) v = __fadd_rn(v, t[q][s2]);
+                        const int64_t m = m0 + j0 + q;
+                        if (col >= 0 && m < p.M) {
+                            if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
+                            store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
                         }
                     }
                 }
             }
+            }  // BN <= 32
         }
     }
 
@@ -514,9 +624,9 @@ cudaError_t launch_bn_mode(const GemmParams& p, bool pdl, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         configured |= uint64_t(1) << dev;
     }
-    if (p.ctas <= 0) return cudaSuccess;
+    if (p.units <= 0 || p.grid <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(p.ctas));
+    cfg.gridDim = dim3(unsigned(p.grid));
     cfg.blockDim = dim3(C::kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = stream;

@@ -30,9 +30,10 @@ __host__ __device__ inline uint32_t eal_offset(uint32_t m, uint32_t k) {
 }
 
 // ---------------------------------------------------------------------------
-// K2 schedule. One CTA per (token block, weight tile, K-slice); a plain grid
-// (no clusters: cluster launches cost several us per kernel at decode sizes).
-// Per token block the CTAs are: S8 slices of every sub8 tile (tile-major),
+// K2 schedule. Work UNITS = (token block, weight tile, K-slice), run by a
+// persistent grid of <= #SM CTAs (CTA b takes units b, b + grid, ...; no
+// clusters: cluster launches cost several us per kernel at decode sizes).
+// Per token block the units are: S8 slices of every sub8 tile (tile-major),
 // then S4 slices of every sub4 tile. Decode uses S8 = 2*S4 so every CTA
 // streams about the same bytes (a sub8 group is twice a sub4 group). When an
 // item (tile, token block) is split (S > 1), each slice writes its f32 partial
@@ -59,8 +60,9 @@ struct GemmParams {
     int32_t out_dtype;      // mq_dtype
     int64_t ldy;
     int32_t S8, S4;         // K-slices per sub8 / sub4 item
-    int32_t ctas;           // grid size
-    float* part;            // split-K partial tiles [ctas][BN][128] (slot = CTA index)
+    int32_t units;          // work units (token block x tile x K-slice)
+    int32_t grid;           // persistent CTAs (<= SMs): CTA b runs units b, b + grid, ...
+    float* part;            // split-K partial tiles [units][BN][128] (slot = unit index)
     uint32_t* cnt;          // arrival counters [TB * (T8 + T4)], zero between launches
     int32_t rotate;         // 1: each CTA starts its K loop at a CTA-dependent chunk (FAST modes)
     uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
@@ -70,8 +72,8 @@ struct GemmParams {
     unsigned long long* trace;  // development: per-CTA globaltimer stamps [P][8] (MQ_DBG & 32)
 };
 
-// One CTA's work: rows of `tile` x tokens of block `tb` x groups [g0, g1);
-// slice `sl` of S; the item's slices are CTAs [cta0, cta0 + S).
+// One unit's work: rows of `tile` x tokens of block `tb` x groups [g0, g1);
+// slice `sl` of S; the item's slices are units [cta0, cta0 + S).
 struct Work {
     int tile, tb, g0, g1, S, sl, cta0, item;
 };
