@@ -52,10 +52,13 @@ struct TcCfg {
     static constexpr int GPS = gemm_gps(BN);                // sub4 groups per chunk
     static constexpr int GPS8 = GPS / 2 > 0 ? GPS / 2 : 1;  // sub8 groups per chunk
     static constexpr int kRaw0 = GPS * kBlock4Bytes > GPS8 * kBlock8Bytes ? GPS * kBlock4Bytes : GPS8 * kBlock8Bytes;
-    static constexpr int kRaw = (kRaw0 + 1023) / 1024 * 1024;
-    static constexpr int kOffB = kRaw;                     // [GPS][BN][128] int8, SW128
-    static constexpr int kOffSa = kOffB + GPS * BN * 128;  // [GPS][BN] f32
-    static constexpr int kStageBytes = ((kOffSa + GPS * BN * 4) + 1023) / 1024 * 1024;
+    // weight stage: one chunk's code+meta blocks; activation stage (separate
+    // ring, so a sub4 weight stage is free as soon as the converter has read it):
+    // the chunk's [GPS][BN][128] SW128 activation tiles + [GPS][BN] f32 scales
+    static constexpr int kStageBytes = (kRaw0 + 1023) / 1024 * 1024;
+    static constexpr int kOffSa = GPS * BN * 128;
+    static constexpr int kXStageBytes = ((kOffSa + GPS * BN * 4) + 1023) / 1024 * 1024;
+    static constexpr int NX = 4;  // activation stages
     // TMEM rings (512 columns): NT accumulator chunk slots of GPS x BN int32
     // columns, NA A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
@@ -70,7 +73,7 @@ struct TcCfg {
     // meta ring (per accumulator slot): weight scales [GPS][128] + act scales [GPS][BN]
     static constexpr int kMetaSlot = GPS * (128 + BN) * 4;
     static constexpr int kMetaBytes = NT * kMetaSlot;
-    static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/ + kMetaBytes;
+    static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/ + kMetaBytes + NX * kXStageBytes;
     static constexpr int NS0 = (kSmemMax - kFixed) / kStageBytes;
 #ifndef MQ_NS_MAX
 #define MQ_NS_MAX 8
@@ -165,12 +168,15 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     // 1024-B aligned base (SWIZZLE_128B atoms), derived from smem_raw so the
     // compiler keeps shared-space provenance (LDS/STS, not generic LD/ST)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* stages = smem;  // [NS][kStageBytes]
-    float* meta = reinterpret_cast<float*>(stages + NS * C::kStageBytes);  // [NT] x (sw [GPS][128] | sa [GPS][BN])
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stages + NS * C::kStageBytes + C::kMetaBytes);
+    uint8_t* stages = smem;                            // [NS][kStageBytes] weights
+    uint8_t* xstages = stages + NS * C::kStageBytes;   // [NX][kXStageBytes] activations
+    float* meta = reinterpret_cast<float*>(xstages + C::NX * C::kXStageBytes);  // [NT] x (sw [GPS][128] | sa [GPS][BN])
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(meta) + C::kMetaBytes);
     uint64_t* full = bars;                 // [NS] producer (expect_tx)
-    uint64_t* empty = full + NS;           // [NS] MMA commit + converter warps
-    uint64_t* afull = empty + NS;          // [NA] converter -> MMA (TMEM A tiles + meta written)
+    uint64_t* empty = full + NS;           // [NS] converter warps + (sub8: MMA commit, sub4: converter)
+    uint64_t* xfull = empty + NS;          // [NX] producer (activation tiles + scales, expect_tx)
+    uint64_t* xempty = xfull + C::NX;      // [NX] MMA commit
+    uint64_t* afull = xempty + C::NX;      // [NA] converter -> MMA (TMEM A tiles + meta written)
     uint64_t* aempty = afull + NA;         // [NA] MMA commit -> converter
     uint64_t* tfull = aempty + NA;         // [NT] MMA commit -> epilogue
     uint64_t* tempty = tfull + NT;         // [NT] epilogue -> MMA / converter (acc + meta slot free)
@@ -181,11 +187,16 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto stage = [&](int s) { return stages + s * C::kStageBytes; };
+    auto xstage = [&](int s) { return xstages + s * C::kXStageBytes; };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1 + 4 * NC);
+        }
+        for (int s = 0; s < C::NX; ++s) {
+            ptx::mbar_init(&xfull[s], 1);
+            ptx::mbar_init(&xempty[s], 1);
         }
         for (int i = 0; i < NA; ++i) {
             ptx::mbar_init(&afull[i], 4 * NC);
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 griddep_wait();
                 if (lane == 0) trace(p, 2);
             }
-            Ring rr;
+            Ring rr, rx;
             int n = 0;  // chunk counter across units
             for (int u = u0; u < p.units; u += ustep) {
                 const Unit U = unit_at(u);
@@ -254,41 +265,43 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                     if (pass == 0 && !pre) break;
                     int gc, cg;
                     chunk_at(U, i, gc, cg);
-                    uint8_t* st = stage(rr.idx);
                     if (pass == 0 || !pre) {
+                        uint8_t* st = stage(rr.idx);
                         if (pass == 1) ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
                         if (lane == 0) trace_chunk(p, 0, n);
                         const uint32_t wbytes = uint32_t(cg * U.ti.blk);
-                        const uint32_t abytes = uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0));
                         if (elect_one()) {
-                            ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes + abytes);
+                            ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes);
                             ptx::bulk_g2s(st, p.wq + U.ti.off + int64_t(gc) * U.ti.blk, wbytes, &full[rr.idx], pol_w);
                         }
                         __syncwarp();
                     }
+                    rr.next<NS>();
                     if (pass == 1) {
+                        uint8_t* xs = xstage(rx.idx);
+                        ptx::mbar_wait(&xempty[rx.idx], rx.ph ^ 1u);
                         if (elect_one()) {
+                            ptx::mbar_arrive_expect_tx(&xfull[rx.idx], uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0)));
                             const int64_t row0 = int64_t(U.wk.tb) * BN;
                             if (contig) {
-                                ptx::bulk_g2s(st + C::kOffB, p.acts + int64_t(gc) * p.Mpad * 128, uint32_t(cg * BN * 128),
-                                              &full[rr.idx], pol_a);
+                                ptx::bulk_g2s(xs, p.acts + int64_t(gc) * p.Mpad * 128, uint32_t(cg * BN * 128),
+                                              &xfull[rx.idx], pol_a);
                                 if (kSa)
-                                    ptx::bulk_g2s(st + C::kOffSa, p.sa + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4),
-                                                  &full[rr.idx], pol_a);
+                                    ptx::bulk_g2s(xs + C::kOffSa, p.sa + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4),
+                                                  &xfull[rx.idx], pol_a);
                             } else {
                                 for (int j = 0; j < cg; ++j) {
-                                    ptx::bulk_g2s(st + C::kOffB + j * BN * 128,
-                                                  p.acts + (int64_t(gc + j) * p.Mpad + row0) * 128, uint32_t(BN * 128),
-                                                  &full[rr.idx], pol_a);
+                                    ptx::bulk_g2s(xs + j * BN * 128, p.acts + (int64_t(gc + j) * p.Mpad + row0) * 128,
+                                                  uint32_t(BN * 128), &xfull[rx.idx], pol_a);
                                     if (kSa)
-                                        ptx::bulk_g2s(st + C::kOffSa + j * BN * 4, p.sa + int64_t(gc + j) * p.Mpad + row0,
-                                                      uint32_t(BN * 4), &full[rr.idx], pol_a);
+                                        ptx::bulk_g2s(xs + C::kOffSa + j * BN * 4, p.sa + int64_t(gc + j) * p.Mpad + row0,
+                                                      uint32_t(BN * 4), &xfull[rx.idx], pol_a);
                                 }
                             }
                         }
                         __syncwarp();
+                        rx.next<C::NX>();
                     }
-                    rr.next<NS>();
                 }
             }
         }
@@ -302,24 +315,28 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
         const uint32_t idesc4 = idesc_i8(BN, true, true);
         const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
-        Ring rs, ra, rt;
+        Ring rs, ra, rt, rx;
         int n = 0;
         for (int u = u0; u < p.units; u += ustep) {
             const Unit U = unit_at(u);
             for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
-                ptx::mbar_wait(&full[rs.idx], rs.ph);
+                // the weight stage is read here only for sub8 chunks (A in SMEM);
+                // sub4 weight stages are released by the converter alone
+                if (U.ti.is8) ptx::mbar_wait(&full[rs.idx], rs.ph);
+                ptx::mbar_wait(&xfull[rx.idx], rx.ph);
                 ptx::mbar_wait(&afull[ra.idx], ra.ph);
                 ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
                 ptx::tc_fence_after();
                 if (lane == 0) trace_chunk(p, 1, n);
                 const uint32_t st = ptx::smem_u32(stage(rs.idx));
+                const uint32_t xs = ptx::smem_u32(xstage(rx.idx));
                 if (elect_one()) {
                     if (!(p.dbg & 4)) {
                         for (int j = 0; j < cg; ++j) {
                             const uint32_t d_tmem = tmem_base + uint32_t((rt.idx * GPS + j) * BN);
-                            const uint32_t b_addr = st + C::kOffB + j * (BN * 128);
+                            const uint32_t b_addr = xs + j * (BN * 128);
                             if (U.ti.is8) {
                                 const uint32_t a_addr = st + j * kBlock8Bytes;
 #pragma unroll
@@ -337,13 +354,15 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                     }
                     ptx::tc_commit(&tfull[rt.idx]);
                     ptx::tc_commit(&aempty[ra.idx]);
-                    ptx::tc_commit(&empty[rs.idx]);
+                    ptx::tc_commit(&xempty[rx.idx]);
+                    if (U.ti.is8) ptx::tc_commit(&empty[rs.idx]);
                 }
                 __syncwarp();
                 if (lane == 0) trace_chunk(p, 2, n);
                 ra.next<NA>();
                 rt.next<NT>();
                 rs.next<NS>();
+                rx.next<C::NX>();
             }
         }
     } else if (warp >= 4 && warp < 4 + 4 * NC) {
@@ -353,7 +372,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         ptx::mbar_wait(tmem_ready, 0);
         ptx::tc_fence_after();
         const uint32_t tmem_row = *reinterpret_cast<volatile uint32_t*>(tmem_holder) + (uint32_t((warp & 3) * 32) << 16);
-        Ring rs, ra, rt;
+        Ring rs, ra, rt, rx;
         int n = 0;
         for (int u = u0; u < p.units; u += ustep) {
             const Unit U = unit_at(u);
@@ -389,7 +408,10 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                         msw[j * 128 + r] = reinterpret_cast<const float*>(st + j * kBlock8Bytes + kCodes8Bytes)[r];
                     }
                 }
-                if (kSa && wg == 0 && r < cg * BN) msw[GPS * 128 + r] = reinterpret_cast<const float*>(st + C::kOffSa)[r];
+                if (kSa && wg == 0) {
+                    ptx::mbar_wait(&xfull[rx.idx], rx.ph);
+                    if (r < cg * BN) msw[GPS * 128 + r] = reinterpret_cast<const float*>(xstage(rx.idx) + C::kOffSa)[r];
+                }
                 if (!U.ti.is8) ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -397,11 +419,14 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                     ptx::mbar_arrive(&mfull[rt.idx]);
                     ptx::mbar_arrive(&afull[ra.idx]);
                     ptx::mbar_arrive(&empty[rs.idx]);
+                    // sub4: the weight stage has no other reader — stand in for the MMA's arrival
+                    if (!U.ti.is8 && threadIdx.x == 128) ptx::mbar_arrive(&empty[rs.idx]);
                 }
                 if (threadIdx.x == 128) trace_chunk(p, 3, n);
                 ra.next<NA>();
                 rt.next<NT>();
                 rs.next<NS>();
+                rx.next<C::NX>();
             }
         }
     } else if (int(threadIdx.x) >= C::kEpiThread0) {
