@@ -271,14 +271,26 @@ def run_ours(args):
     e2e = None
     if world == 1:
         xs, ys = head["xs"], head["ys"]
-        hx = [x.cpu().pin_memory() for x in xs]
-        hy = [torch.empty(y.shape, dtype=y.dtype).pin_memory() for y in ys]
+        # one pinned input buffer (every layer's activations) and one output
+        # buffer: one H2D and one D2H copy per step
+        nx = [x.numel() for x in xs]
+        ny = [y.numel() for y in ys]
+        hx_all = torch.cat([x.reshape(-1).cpu() for x in xs]).pin_memory()
+        dx_all = torch.empty(sum(nx), dtype=torch.float32, device=dev)
+        dy_all = torch.empty(sum(ny), dtype=ys[0].dtype, device=dev)
+        hy_all = torch.empty(sum(ny), dtype=ys[0].dtype).pin_memory()
+        xv = list(torch.split(dx_all, nx))
+        yv = list(torch.split(dy_all, ny))
+        xv = [v.view(x.shape) for v, x in zip(xv, xs)]
+        yv = [v.view(y.shape) for v, y in zip(yv, ys)]
+        hx = [hx_all]
+        hy = [hy_all]
 
         def e2e_step(r):
+            dx_all.copy_(hx_all, non_blocking=True)
             for i in range(len(host)):
-                xs[i].copy_(hx[i], non_blocking=True)
-                layers[r][i].forward(xs[i], out=ys[i], opts=head["opts"])
-                hy[i].copy_(ys[i], non_blocking=True)
+                layers[r][i].forward(xv[i], out=yv[i], opts=head["opts"])
+            hy_all.copy_(dy_all, non_blocking=True)
 
         efns = graphs_for(e2e_step)
         ems = timed(efns, args.steps, args.warmup)

@@ -123,9 +123,9 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
 
 // Forward workspace: split-K arrival counters (zero between launches; the
 // kernel re-arms them) | split-K partial tiles | EAL codes [G][Mpad][128] |
-// EAL scales [Ga][Mpad].
+// EAL scales [Ga][Mpad] | EAL code sums [G][Mpad] int32.
 struct EalWs {
-    size_t off_part, off_acts, off_sa, total;
+    size_t off_part, off_acts, off_sa, off_asum, total;
 };
 EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
@@ -136,7 +136,8 @@ EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
     w.off_acts = w.off_part + (split ? al(size_t(pl.units) * 128 * size_t(pl.bn) * 4) : 0);
     w.off_sa = w.off_acts + al(size_t(L->G) * size_t(pl.Mpad) * 128);
     const int64_t Ga = pl.per_token ? 1 : L->G;
-    w.total = w.off_sa + al(size_t(Ga) * size_t(pl.Mpad) * 4);
+    w.off_asum = w.off_sa + al(size_t(Ga) * size_t(pl.Mpad) * 4);
+    w.total = w.off_asum + al(size_t(L->G) * size_t(pl.Mpad) * 4);
     return w;
 }
 
@@ -386,6 +387,7 @@ mq_status launch_k2(mq_layer_s* L, const Plan& pl, const void* ws, int64_t M, vo
     p.part = reinterpret_cast<float*>(base + w.off_part);
     p.acts = base + w.off_acts;
     p.sa = reinterpret_cast<const float*>(base + w.off_sa);
+    p.asum = reinterpret_cast<const int32_t*>(base + w.off_asum);
     cudaError_t e = launch_mixed_gemm_tc(p, pl.bn, pl.mode, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "mixed_gemm launch");
     return MQ_OK;
@@ -420,7 +422,8 @@ mq_status mq_mixed_linear_codes(mq_layer_t L, const int8_t* codes, int64_t ldc, 
     }
     uint8_t* acts = static_cast<uint8_t*>(ws) + w.off_acts;
     float* sa = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + w.off_sa);
-    cudaError_t e = launch_repack_eal(codes, ldc, scales, lds, pl.per_token, M, L->K, pl.Mpad, acts, sa, s);
+    int32_t* asum = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + w.off_asum);
+    cudaError_t e = launch_repack_eal(codes, ldc, scales, lds, pl.per_token, M, L->K, pl.Mpad, acts, sa, asum, s);
     if (e != cudaSuccess) return cuda_fail(e, "repack launch");
     return launch_k2(L, pl, ws, M, Y, out_dtype, s);
 }
@@ -446,8 +449,9 @@ mq_status mq_mixed_linear(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t
     uint8_t* acts = static_cast<uint8_t*>(ws) + w.off_acts;
     float* sa = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + w.off_sa);
     if (o && o->gemm_impl == 1) return fail(MQ_USAGE, "the SIMT debug kernel takes quantized codes (mq_mixed_linear_codes)");
+    int32_t* asum = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + w.off_asum);
     cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad, acts,
-                                         sa, err, pl.pdl, s);
+                                         sa, asum, err, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
     return launch_k2(L, pl, ws, M, Y, out_dtype, s);
 }
@@ -463,7 +467,8 @@ mq_status mq_quantize_act_ws(mq_layer_t L, const void* A, mq_dtype a_dtype, int6
     const EalWs w = eal_ws_layout(L, pl);
     uint8_t* base = static_cast<uint8_t*>(ws);
     cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad,
-                                         base + w.off_acts, reinterpret_cast<float*>(base + w.off_sa), err, pl.pdl,
+                                         base + w.off_acts, reinterpret_cast<float*>(base + w.off_sa),
+                                         reinterpret_cast<int32_t*>(base + w.off_asum), err, pl.pdl,
                                          static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
     return MQ_OK;
@@ -501,12 +506,14 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
     float* sa = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + w.off_sa);
     // scales are unused by the dump: repack with zero scales from a null-free buffer
     cudaError_t e = cudaMemsetAsync(sa, 0, w.total - w.off_sa, s);
-    if (e == cudaSuccess) e = launch_repack_eal(codes, ldc, sa, 0, 1, M, L->K, pl.Mpad, acts, sa, s);
+    int32_t* asum = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + w.off_asum);
+    if (e == cudaSuccess) e = launch_repack_eal(codes, ldc, sa, 0, 1, M, L->K, pl.Mpad, acts, sa, asum, s);
     if (e != cudaSuccess) return cuda_fail(e, "repack launch");
     GemmParams p;
     gemm_params(L, pl, M, nullptr, MQ_F32, &p);
     p.acts = acts;
     p.sa = sa;
+    p.asum = asum;
     // restrict the launch to one sub-problem: its tiles, offsets and rows
     if (which == 0) {
         p.T4 = 0;

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) act_quant_row_kernel(
 template <int DT>
 __global__ void act_quant_eal_group_kernel(const void* __restrict__ A, int64_t M, int64_t K, int64_t lda, int G,
                                            int64_t Mpad, uint8_t* __restrict__ acts, float* __restrict__ sa,
-                                           int32_t* err) {
+                                           int32_t* __restrict__ asum, int32_t* err) {
     griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
     griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -159,15 +159,24 @@ __global__ void act_quant_eal_group_kernel(const void* __restrict__ A, int64_t M
     finite = __all_sync(0xffffffffu, finite);
     uint32_t word = 0;
     float s = 0.0f;
+    int csum = 0;
     if (m < M) {
         if (!finite && lane == 0 && err) atomicMin(err, static_cast<int32_t>(m * G + g));
         s = act_scale(amax, 0);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            if (4 * lane + i < len) word |= uint32_t(uint8_t(quant_one(x[i], s))) << (8 * i);
+            if (4 * lane + i < len) {
+                const int8_t c = quant_one(x[i], s);
+                csum += c;
+                word |= uint32_t(uint8_t(c)) << (8 * i);
+            }
     }
+    for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
     *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(4 * lane))) = word;
-    if (lane == 0) sa[int64_t(g) * Mpad + m] = s;
+    if (lane == 0) {
+        sa[int64_t(g) * Mpad + m] = s;
+        asum[int64_t(g) * Mpad + m] = csum;  // sum of the group's codes: the zero-point correction term
+    }
 }
 
 // per-token (group == K): one CTA per token row m < Mpad
@@ -175,7 +184,7 @@ template <int DT>
 __global__ void __launch_bounds__(256) act_quant_eal_row_kernel(const void* __restrict__ A, int64_t M, int64_t K,
                                                                 int64_t lda, int G, int64_t Mpad,
                                                                 uint8_t* __restrict__ acts, float* __restrict__ sa,
-                                                                int32_t* err) {
+                                                                int32_t* __restrict__ asum, int32_t* err) {
     griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
     griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     __shared__ float red[8];
@@ -206,18 +215,29 @@ __global__ void __launch_bounds__(256) act_quant_eal_row_kernel(const void* __re
     }
     if (live && anybad && threadIdx.x == 0 && err) atomicMin(err, static_cast<int32_t>(m));
     const float s = live ? act_scale(amax, 0) : 0.0f;
-    // 4 codes per thread-iteration, all G groups of this row
-    for (int64_t q = threadIdx.x; q < int64_t(G) * 32; q += blockDim.x) {
+    // 4 codes per thread-iteration, all G groups of this row; a warp covers one
+    // group per iteration (blockDim is a multiple of 32), so it also sums it
+    const int64_t qend = (int64_t(G) * 32 + blockDim.x - 1) / blockDim.x * blockDim.x;
+    for (int64_t q = threadIdx.x; q < qend; q += blockDim.x) {
         const int g = static_cast<int>(q >> 5);
         const int k0 = static_cast<int>(q & 31) * 4;
         uint32_t word = 0;
-        if (live)
+        int csum = 0;
+        if (live && g < G)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int64_t k = int64_t(g) * 128 + k0 + i;
-                if (k < K) word |= uint32_t(uint8_t(quant_one(load_act<DT>(A, m * lda + k), s))) << (8 * i);
+                if (k < K) {
+                    const int8_t c = quant_one(load_act<DT>(A, m * lda + k), s);
+                    csum += c;
+                    word |= uint32_t(uint8_t(c)) << (8 * i);
+                }
             }
-        *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(k0))) = word;
+        for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+        if (g < G) {
+            *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(k0))) = word;
+            if ((threadIdx.x & 31) == 0) asum[int64_t(g) * Mpad + m] = csum;
+        }
     }
     if (threadIdx.x == 0) sa[m] = s;
 }
@@ -225,20 +245,30 @@ __global__ void __launch_bounds__(256) act_quant_eal_row_kernel(const void* __re
 // row-major codes/scales (reference layout) -> EAL; one thread per 4 codes
 __global__ void repack_eal_kernel(const int8_t* __restrict__ codes, int64_t ldc, const float* __restrict__ scales,
                                   int64_t lds, int per_token, int64_t M, int64_t K, int G, int64_t Mpad,
-                                  uint8_t* __restrict__ acts, float* __restrict__ sa) {
-    const int64_t total = int64_t(G) * Mpad * 32;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(i / (Mpad * 32));
+                                  uint8_t* __restrict__ acts, float* __restrict__ sa, int32_t* __restrict__ asum) {
+    const int64_t total = int64_t(G) * Mpad * 32;  // a multiple of 32: warps stay aligned to one (g, m)
+    const int64_t tend = (total + int64_t(gridDim.x) * blockDim.x - 1) / (int64_t(gridDim.x) * blockDim.x) *
+                         (int64_t(gridDim.x) * blockDim.x);
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < tend; i += int64_t(gridDim.x) * blockDim.x) {
+        const bool in = i < total;
+        const int g = in ? static_cast<int>(i / (Mpad * 32)) : 0;
         const int64_t rem = i - int64_t(g) * Mpad * 32;
         const int64_t m = rem >> 5;
         const int k0 = static_cast<int>(rem & 31) * 4;
         uint32_t word = 0;
-        if (m < M)
+        int csum = 0;
+        if (in && m < M)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int64_t k = int64_t(g) * 128 + k0 + j;
-                if (k < K) word |= uint32_t(uint8_t(codes[m * ldc + k])) << (8 * j);
+                if (k < K) {
+                    csum += codes[m * ldc + k];
+                    word |= uint32_t(uint8_t(codes[m * ldc + k])) << (8 * j);
+                }
             }
+        for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+        if (!in) continue;
+        if (k0 == 0) asum[int64_t(g) * Mpad + m] = csum;
         *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(k0))) = word;
         if (k0 == 0) {
             if (per_token) {
@@ -267,34 +297,35 @@ cudaError_t launch_ex(K kern, dim3 grid, dim3 block, bool pdl, cudaStream_t stre
 }  // namespace
 
 cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda, int group,
-                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* err, bool pdl,
+                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum, int32_t* err, bool pdl,
                                  cudaStream_t stream) {
     if (Mpad == 0) return cudaSuccess;
     const int G = static_cast<int>((K + 127) / 128);
     if (group >= K) {
         const dim3 grid(static_cast<unsigned>(Mpad));
         switch (a_dtype) {
-            case 0: return launch_ex(act_quant_eal_row_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
-            case 1: return launch_ex(act_quant_eal_row_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
-            default: return launch_ex(act_quant_eal_row_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+            case 0: return launch_ex(act_quant_eal_row_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
+            case 1: return launch_ex(act_quant_eal_row_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
+            default: return launch_ex(act_quant_eal_row_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
         }
     }
     const int64_t warps = Mpad * G;
     const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));
     switch (a_dtype) {
-        case 0: return launch_ex(act_quant_eal_group_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
-        case 1: return launch_ex(act_quant_eal_group_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
-        default: return launch_ex(act_quant_eal_group_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, err);
+        case 0: return launch_ex(act_quant_eal_group_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
+        case 1: return launch_ex(act_quant_eal_group_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
+        default: return launch_ex(act_quant_eal_group_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
     }
 }
 
 cudaError_t launch_repack_eal(const int8_t* codes, int64_t ldc, const float* scales, int64_t lds, int per_token,
-                              int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, cudaStream_t stream) {
+                              int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum,
+                              cudaStream_t stream) {
     const int G = static_cast<int>((K + 127) / 128);
     const int64_t total = int64_t(G) * Mpad * 32;
     if (total == 0) return cudaSuccess;
     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
-    repack_eal_kernel<<<grid, 256, 0, stream>>>(codes, ldc, scales, lds, per_token, M, K, G, Mpad, acts, sa);
+    repack_eal_kernel<<<grid, 256, 0, stream>>>(codes, ldc, scales, lds, per_token, M, K, G, Mpad, acts, sa, asum);
     return cudaGetLastError();
 }
 

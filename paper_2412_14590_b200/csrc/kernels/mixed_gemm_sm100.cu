@@ -56,9 +56,14 @@ struct TcCfg {
     // ring, so a sub4 weight stage is free as soon as the converter has read it):
     // the chunk's [GPS][BN][128] SW128 activation tiles + [GPS][BN] f32 scales
     static constexpr int kStageBytes = (kRaw0 + 1023) / 1024 * 1024;
+    // decode token tiles apply the sub4 zero point in the epilogue
+    // (sum a(c - z) = sum a c - z sum a, sum a from K1), so the converter only
+    // widens nibbles to bytes and the MMA reads the codes as u8
+    static constexpr bool kZpEpi = BN <= 32;
     static constexpr int kOffSa = GPS * BN * 128;
-    static constexpr int kXStageBytes = ((kOffSa + GPS * BN * 4) + 1023) / 1024 * 1024;
-    static constexpr int NX = 4;  // activation stages
+    static constexpr int kOffAs = kOffSa + GPS * BN * 4;
+    static constexpr int kXStageBytes = ((kOffAs + (kZpEpi ? GPS * BN * 4 : 0)) + 1023) / 1024 * 1024;
+    static constexpr int NX = 3;  // activation stages
     // TMEM rings (512 columns): NT accumulator chunk slots of GPS x BN int32
     // columns, NA A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
@@ -70,16 +75,23 @@ struct TcCfg {
     static constexpr uint32_t kTmemNeed = kAccCols + NA * kAPerChunk;
     static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
     static_assert(kTmemNeed <= 512 && NA >= 2, "TMEM budget");
-    // meta ring (per accumulator slot): weight scales [GPS][128] + act scales [GPS][BN]
-    static constexpr int kMetaSlot = GPS * (128 + BN) * 4;
-    static constexpr int kMetaBytes = NT * kMetaSlot;
+    // meta ring (per accumulator slot): weight scales [GPS][128] | (kZpEpi) zero
+    // points [GPS][128] | act scales [GPS][BN] | (kZpEpi) code sums [GPS][BN]
+    static constexpr int kMetaZp = GPS * 128, kMetaSa = GPS * 128 * (kZpEpi ? 2 : 1), kMetaAs = kMetaSa + GPS * BN;
+    static constexpr int kMetaSlot = (kMetaAs + (kZpEpi ? GPS * BN : 0)) * 4;
+    // the meta ring is deeper than the accumulator ring and has its own
+    // barriers, so the converter never waits on the epilogue of chunk n - NT
+    static constexpr int NM = 4;
+    static constexpr int kMetaBytes = NM * kMetaSlot;
     static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/ + kMetaBytes + NX * kXStageBytes;
     static constexpr int NS0 = (kSmemMax - kFixed) / kStageBytes;
 #ifndef MQ_NS_MAX
 #define MQ_NS_MAX 8
 #endif
     static constexpr int NS = NS0 > MQ_NS_MAX ? MQ_NS_MAX : NS0;
-    static constexpr int NE = BN <= 64 ? 1 : 2;  // epilogue warpgroups
+    // epilogue warpgroups: two at decode too — one warp per SMSP would leave the
+    // TMEM-load / rescale chain latency-bound
+    static constexpr int NE = (BN <= 32 || BN >= 128) ? 2 : 1;
     static constexpr int NC = BN <= 32 ? 2 : 1;  // converter warpgroups (decode is conversion-bound)
     static constexpr int BNE = BN / NE;          // tokens per epilogue warpgroup
     static constexpr int kEpiThread0 = 128 * (1 + NC);
@@ -180,8 +192,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     uint64_t* aempty = afull + NA;         // [NA] MMA commit -> converter
     uint64_t* tfull = aempty + NA;         // [NT] MMA commit -> epilogue
     uint64_t* tempty = tfull + NT;         // [NT] epilogue -> MMA / converter (acc + meta slot free)
-    uint64_t* mfull = tempty + NT;         // [NT] converter -> epilogue (meta slot written)
-    uint64_t* tmem_ready = mfull + NT;     // warp 1 -> everyone using TMEM
+    uint64_t* mfull = tempty + NT;         // [NM] converter -> epilogue (meta slot written)
+    uint64_t* mempty = mfull + C::NM;      // [NM] epilogue -> converter (meta slot read)
+    uint64_t* tmem_ready = mempty + C::NM; // warp 1 -> everyone using TMEM
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_ready + 1);
     volatile int* s_last = reinterpret_cast<volatile int*>(tmem_holder + 1);  // split-K: this CTA reduces
 
@@ -205,7 +218,10 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         for (int i = 0; i < NT; ++i) {
             ptx::mbar_init(&tfull[i], 1);
             ptx::mbar_init(&tempty[i], 4 * NE);
+        }
+        for (int i = 0; i < C::NM; ++i) {
             ptx::mbar_init(&mfull[i], 4 * NC);
+            ptx::mbar_init(&mempty[i], 4 * NE);
         }
         ptx::mbar_init(tmem_ready, 1);
         ptx::fence_barrier_init();
@@ -244,65 +260,72 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
 
     if (warp == 0) {
         // ============================== producer ==============================
+        if (lane == 0) trace(p, 2);
         const uint64_t pol_w = ptx::policy_evict_first();
+        // weights are immutable: this warp never waits on the previous kernel
+        // (griddepcontrol), so under PDL the first NS stages fill while it runs
+        Ring rr;
+        int n = 0;  // chunk counter across units
+        for (int u = u0; u < p.units; u += ustep) {
+            const Unit U = unit_at(u);
+            for (int i = 0; i < U.nch; ++i, ++n) {
+                int gc, cg;
+                chunk_at(U, i, gc, cg);
+                uint8_t* st = stage(rr.idx);
+                ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
+                if (lane == 0) trace_chunk(p, 0, n);
+                if (n == 0 && lane == 0) trace(p, 7);
+                const uint32_t wbytes = uint32_t(cg * U.ti.blk);
+                if (elect_one()) {
+                    ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes);
+                    ptx::bulk_g2s(st, p.wq + U.ti.off + int64_t(gc) * U.ti.blk, wbytes, &full[rr.idx], pol_w);
+                }
+                __syncwarp();
+                rr.next<NS>();
+            }
+        }
+        if (lane == 0) trace(p, 1);
+    } else if (warp == 2) {
+        // ===================== activation producer (EAL tiles) =====================
+        // its own warp, so the weight stream never waits behind the activation ring
         const uint64_t pol_a = ptx::policy_evict_last();
         const bool contig = p.Mpad == BN;  // one token tile: a chunk's act tiles are contiguous
-        // pass 0: weights of the first NS chunks (independent of the previous
-        // kernel); pass 1: activations/scales + everything else.
-        for (int pass = 0; pass < 2; ++pass) {
-            if (pass == 1) {
-                if (lane == 0) trace(p, 1);
-                griddep_wait();
-                if (lane == 0) trace(p, 2);
-            }
-            Ring rr, rx;
-            int n = 0;  // chunk counter across units
-            for (int u = u0; u < p.units; u += ustep) {
-                const Unit U = unit_at(u);
-                if (pass == 0 && n >= NS) break;
-                for (int i = 0; i < U.nch; ++i, ++n) {
-                    const bool pre = n < NS;
-                    if (pass == 0 && !pre) break;
-                    int gc, cg;
-                    chunk_at(U, i, gc, cg);
-                    if (pass == 0 || !pre) {
-                        uint8_t* st = stage(rr.idx);
-                        if (pass == 1) ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
-                        if (lane == 0) trace_chunk(p, 0, n);
-                        const uint32_t wbytes = uint32_t(cg * U.ti.blk);
-                        if (elect_one()) {
-                            ptx::mbar_arrive_expect_tx(&full[rr.idx], wbytes);
-                            ptx::bulk_g2s(st, p.wq + U.ti.off + int64_t(gc) * U.ti.blk, wbytes, &full[rr.idx], pol_w);
+        griddep_wait();  // K1's output
+        Ring rx;
+        for (int u = u0; u < p.units; u += ustep) {
+            const Unit U = unit_at(u);
+            for (int i = 0; i < U.nch; ++i) {
+                int gc, cg;
+                chunk_at(U, i, gc, cg);
+                uint8_t* xs = xstage(rx.idx);
+                ptx::mbar_wait(&xempty[rx.idx], rx.ph ^ 1u);
+                if (elect_one()) {
+                    ptx::mbar_arrive_expect_tx(&xfull[rx.idx], uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0) +
+                                                                        (C::kZpEpi ? cg * BN * 4 : 0)));
+                    const int64_t row0 = int64_t(U.wk.tb) * BN;
+                    if (contig) {
+                        ptx::bulk_g2s(xs, p.acts + int64_t(gc) * p.Mpad * 128, uint32_t(cg * BN * 128), &xfull[rx.idx], pol_a);
+                        if (kSa)
+                            ptx::bulk_g2s(xs + C::kOffSa, p.sa + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4), &xfull[rx.idx],
+                                          pol_a);
+                        if (C::kZpEpi)
+                            ptx::bulk_g2s(xs + C::kOffAs, p.asum + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4),
+                                          &xfull[rx.idx], pol_a);
+                    } else {
+                        for (int j = 0; j < cg; ++j) {
+                            ptx::bulk_g2s(xs + j * BN * 128, p.acts + (int64_t(gc + j) * p.Mpad + row0) * 128,
+                                          uint32_t(BN * 128), &xfull[rx.idx], pol_a);
+                            if (kSa)
+                                ptx::bulk_g2s(xs + C::kOffSa + j * BN * 4, p.sa + int64_t(gc + j) * p.Mpad + row0,
+                                              uint32_t(BN * 4), &xfull[rx.idx], pol_a);
+                            if (C::kZpEpi)
+                                ptx::bulk_g2s(xs + C::kOffAs + j * BN * 4, p.asum + int64_t(gc + j) * p.Mpad + row0,
+                                              uint32_t(BN * 4), &xfull[rx.idx], pol_a);
                         }
-                        __syncwarp();
-                    }
-                    rr.next<NS>();
-                    if (pass == 1) {
-                        uint8_t* xs = xstage(rx.idx);
-                        ptx::mbar_wait(&xempty[rx.idx], rx.ph ^ 1u);
-                        if (elect_one()) {
-                            ptx::mbar_arrive_expect_tx(&xfull[rx.idx], uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0)));
-                            const int64_t row0 = int64_t(U.wk.tb) * BN;
-                            if (contig) {
-                                ptx::bulk_g2s(xs, p.acts + int64_t(gc) * p.Mpad * 128, uint32_t(cg * BN * 128),
-                                              &xfull[rx.idx], pol_a);
-                                if (kSa)
-                                    ptx::bulk_g2s(xs + C::kOffSa, p.sa + int64_t(gc) * p.Mpad, uint32_t(cg * BN * 4),
-                                                  &xfull[rx.idx], pol_a);
-                            } else {
-                                for (int j = 0; j < cg; ++j) {
-                                    ptx::bulk_g2s(xs + j * BN * 128, p.acts + (int64_t(gc + j) * p.Mpad + row0) * 128,
-                                                  uint32_t(BN * 128), &xfull[rx.idx], pol_a);
-                                    if (kSa)
-                                        ptx::bulk_g2s(xs + C::kOffSa + j * BN * 4, p.sa + int64_t(gc + j) * p.Mpad + row0,
-                                                      uint32_t(BN * 4), &xfull[rx.idx], pol_a);
-                                }
-                            }
-                        }
-                        __syncwarp();
-                        rx.next<C::NX>();
                     }
                 }
+                __syncwarp();
+                rx.next<C::NX>();
             }
         }
     } else if (warp == 1) {
@@ -313,7 +336,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         if (lane == 0) ptx::mbar_arrive(tmem_ready);
         ptx::tc_fence_after();
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
-        const uint32_t idesc4 = idesc_i8(BN, true, true);
+        const uint32_t idesc4 = idesc_i8(BN, !C::kZpEpi, true);  // kZpEpi: raw u4 codes as u8
         const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
         Ring rs, ra, rt, rx;
         int n = 0;
@@ -372,59 +395,95 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         ptx::mbar_wait(tmem_ready, 0);
         ptx::tc_fence_after();
         const uint32_t tmem_row = *reinterpret_cast<volatile uint32_t*>(tmem_holder) + (uint32_t((warp & 3) * 32) << 16);
-        Ring rs, ra, rt, rx;
+        Ring rs, ra, rm, rx;
         int n = 0;
         for (int u = u0; u < p.units; u += ustep) {
             const Unit U = unit_at(u);
             for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
-                // every chunk (sub8 too): wait for the stage, a free A slot and a free
-                // meta slot (a role that skipped chunks could run two phases ahead of
-                // a barrier and read an older phase's parity as complete)
+                // (1) every chunk (sub8 too — a role that skipped chunks could run two
+                // phases ahead of a barrier and read an older phase's parity as
+                // complete): pull this thread's codes / zero point / scale out of the
+                // weight stage into registers and release the stage at once, so the
+                // weight stream never waits for the TMEM rings or the epilogue
+                constexpr int JPW = (GPS + NC - 1) / NC;  // groups per converter warpgroup
                 ptx::mbar_wait(&full[rs.idx], rs.ph);
                 if (threadIdx.x == 128) trace_chunk(p, 5, n);
-                ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
-                ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
-                if (threadIdx.x == 128) trace_chunk(p, 6, n);
                 const uint8_t* st = stage(rs.idx);
-                float* msw = meta + rt.idx * (C::kMetaSlot / 4);
-                for (int j = wg; j < cg; j += NC) {
+                uint4 raw[JPW][4];
+                uint32_t kk[JPW];
+                float swv[JPW];
+#pragma unroll
+                for (int jj = 0; jj < JPW; ++jj) {
+                    const int j = wg + jj * NC;
+                    if (j >= cg) break;
                     if (!U.ti.is8) {
-                        const uint8_t* raw = st + j * kBlock4Bytes;
-                        const uint32_t kk = uint32_t(128 - raw[kCodes4Bytes + 512 + r]) * 0x01010101u;
+                        const uint8_t* blk = st + j * kBlock4Bytes;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) raw[jj][q] = *reinterpret_cast<const uint4*>(blk + q * 2048 + r * 16);
+                        kk[jj] = C::kZpEpi ? uint32_t(blk[kCodes4Bytes + 512 + r])
+                                           : uint32_t(128 - blk[kCodes4Bytes + 512 + r]) * 0x01010101u;
+                        swv[jj] = reinterpret_cast<const float*>(blk + kCodes4Bytes)[r];
+                    } else {
+                        swv[jj] = reinterpret_cast<const float*>(st + j * kBlock8Bytes + kCodes8Bytes)[r];
+                        kk[jj] = 0u;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&empty[rs.idx]);
+                    // sub4: the weight stage has no other reader — stand in for the MMA's arrival
+                    if (!U.ti.is8 && threadIdx.x == 128) ptx::mbar_arrive(&empty[rs.idx]);
+                }
+                // (2) convert into a free TMEM A slot, scales into a free meta slot
+                ptx::mbar_wait(&aempty[ra.idx], ra.ph ^ 1u);
+                ptx::mbar_wait(&mempty[rm.idx], rm.ph ^ 1u);
+                if (threadIdx.x == 128) trace_chunk(p, 6, n);
+                float* msw = meta + rm.idx * (C::kMetaSlot / 4);
+#pragma unroll
+                for (int jj = 0; jj < JPW; ++jj) {
+                    const int j = wg + jj * NC;
+                    if (j >= cg) break;
+                    if (!U.ti.is8) {
                         uint32_t v[32];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const uint4 w = *reinterpret_cast<const uint4*>(raw + q * 2048 + r * 16);
-                            unpack_word(w.x, kk, v[q * 8 + 0], v[q * 8 + 1]);
-                            unpack_word(w.y, kk, v[q * 8 + 2], v[q * 8 + 3]);
-                            unpack_word(w.z, kk, v[q * 8 + 4], v[q * 8 + 5]);
-                            unpack_word(w.w, kk, v[q * 8 + 6], v[q * 8 + 7]);
+                            const uint32_t w4[4] = {raw[jj][q].x, raw[jj][q].y, raw[jj][q].z, raw[jj][q].w};
+#pragma unroll
+                            for (int e2 = 0; e2 < 4; ++e2) {
+                                if constexpr (C::kZpEpi) {  // widen only: bytes c (zero point applied in the epilogue)
+                                    v[q * 8 + 2 * e2] = w4[e2] & 0x0F0F0F0Fu;
+                                    v[q * 8 + 2 * e2 + 1] = (w4[e2] >> 4) & 0x0F0F0F0Fu;
+                                } else {
+                                    unpack_word(w4[e2], kk[jj], v[q * 8 + 2 * e2], v[q * 8 + 2 * e2 + 1]);
+                                }
+                            }
                         }
                         if (!(p.dbg & 2)) ptx::tmem_st32(tmem_row + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32), v);
-                        msw[j * 128 + r] = reinterpret_cast<const float*>(raw + kCodes4Bytes)[r];
-                    } else {
-                        msw[j * 128 + r] = reinterpret_cast<const float*>(st + j * kBlock8Bytes + kCodes8Bytes)[r];
                     }
+                    msw[j * 128 + r] = swv[jj];
+                    if constexpr (C::kZpEpi) reinterpret_cast<int32_t*>(msw)[C::kMetaZp + j * 128 + r] = int32_t(kk[jj]);
                 }
-                if (kSa && wg == 0) {
+                if ((kSa || C::kZpEpi) && wg == 0) {
                     ptx::mbar_wait(&xfull[rx.idx], rx.ph);
-                    if (r < cg * BN) msw[GPS * 128 + r] = reinterpret_cast<const float*>(xstage(rx.idx) + C::kOffSa)[r];
+                    if (r < cg * BN) {
+                        if (kSa) msw[C::kMetaSa + r] = reinterpret_cast<const float*>(xstage(rx.idx) + C::kOffSa)[r];
+                        if constexpr (C::kZpEpi)
+                            reinterpret_cast<int32_t*>(msw)[C::kMetaAs + r] =
+                                reinterpret_cast<const int32_t*>(xstage(rx.idx) + C::kOffAs)[r];
+                    }
                 }
                 if (!U.ti.is8) ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::mbar_arrive(&mfull[rt.idx]);
+                    ptx::mbar_arrive(&mfull[rm.idx]);
                     ptx::mbar_arrive(&afull[ra.idx]);
-                    ptx::mbar_arrive(&empty[rs.idx]);
-                    // sub4: the weight stage has no other reader — stand in for the MMA's arrival
-                    if (!U.ti.is8 && threadIdx.x == 128) ptx::mbar_arrive(&empty[rs.idx]);
                 }
                 if (threadIdx.x == 128) trace_chunk(p, 3, n);
                 ra.next<NA>();
-                rt.next<NT>();
+                rm.next<C::NM>();
                 rs.next<NS>();
                 rx.next<C::NX>();
             }
@@ -440,7 +499,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         ptx::tc_fence_after();
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
         griddep_wait();  // scales / output of this launch are ours now
-        Ring rt;
+        Ring rt, rm;
         int n = 0;
         for (int u = u0; u < p.units; u += ustep) {
             const Unit U = unit_at(u);
@@ -465,22 +524,24 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
             for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
-                ptx::mbar_wait(&mfull[rt.idx], rt.ph);
+                ptx::mbar_wait(&mfull[rm.idx], rm.ph);
                 ptx::mbar_wait(&tfull[rt.idx], rt.ph);
                 ptx::tc_fence_after();
                 if (n == 0 && et == 0) trace(p, 3);
-                const float* msw = meta + rt.idx * (C::kMetaSlot / 4);
-                if constexpr (kPair && BNE == 16) {
-                    // decode: two groups' sums in flight per wait (register budget at 512 threads)
+                const float* msw = meta + rm.idx * (C::kMetaSlot / 4);
+                if constexpr (kPair && (BNE == 16 || BNE == 8)) {
+                    // decode: two groups' sums in flight per wait (register budget)
 #pragma unroll
                     for (int j0 = 0; j0 < GPS; j0 += 2) {
                         if (j0 >= cg || (p.dbg & 1)) break;
-                        uint32_t v[2][16];
+                        uint32_t v[2][BNE];
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
-                            if (j0 + h < cg)
-                                ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + uint32_t((rt.idx * GPS + j0 + h) * BN + c0),
-                                               v[h]);
+                            if (j0 + h < cg) {
+                                const uint32_t ta = tmem_base + (uint32_t(wq * 32) << 16) + uint32_t((rt.idx * GPS + j0 + h) * BN + c0);
+                                if constexpr (BNE == 16) ptx::tmem_ld16(ta, v[h]);
+                                else ptx::tmem_ld8(ta, v[h]);
+                            }
                         ptx::tmem_wait_ld();
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
@@ -488,9 +549,15 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                             const int j = j0 + h;
                             const float sw = msw[j * 128 + r];
                             const uint64_t sw2 = pk2(sw, sw);
-                            const float* sav = msw + GPS * 128 + j * BN + c0;
+                            const float* sav = msw + C::kMetaSa + j * BN + c0;
+                            if constexpr (C::kZpEpi) {  // S = sum a c - z sum a (exact int32)
+                                const int32_t zr = reinterpret_cast<const int32_t*>(msw)[C::kMetaZp + j * 128 + r];
+                                const int32_t* asv = reinterpret_cast<const int32_t*>(msw) + C::kMetaAs + j * BN + c0;
 #pragma unroll
-                            for (int q = 0; q < 16; q += 2) {
+                                for (int q = 0; q < BNE; ++q) v[h][q] = uint32_t(int32_t(v[h][q]) - zr * asv[q]);
+                            }
+#pragma unroll
+                            for (int q = 0; q < BNE; q += 2) {
                                 const uint64_t g2 = pk2(__int2float_rn(int32_t(v[h][q])), __int2float_rn(int32_t(v[h][q + 1])));
                                 if constexpr (MODE == kFastGroup)
                                     acc2[q / 2] = fma2(g2, mul2(*reinterpret_cast<const uint64_t*>(sav + q), sw2), acc2[q / 2]);
@@ -502,20 +569,28 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 } else
                 for (int j = 0; j < cg; ++j) {
                     const float sw = msw[j * 128 + r];
-                    const float* sav = msw + GPS * 128 + j * BN + c0;
+                    const float* sav = msw + C::kMetaSa + j * BN + c0;
                     const uint64_t sw2 = pk2(sw, sw);
                     const uint32_t tcol = uint32_t((rt.idx * GPS + j) * BN + c0);
+                    constexpr int CW = BNE < 16 ? BNE : 16;  // TMEM columns per load
 #pragma unroll
-                    for (int ch = 0; ch < BNE / 16; ++ch) {
+                    for (int ch = 0; ch < BNE / CW; ++ch) {
                         if (p.dbg & 1) break;
-                        uint32_t v[16];
-                        ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * 16, v);
+                        uint32_t v[CW];
+                        if constexpr (CW == 16) ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * 16, v);
+                        else ptx::tmem_ld8(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * CW, v);
                         ptx::tmem_wait_ld();
+                        if constexpr (C::kZpEpi) {  // S = sum a c - z sum a (exact int32)
+                            const int32_t zr = reinterpret_cast<const int32_t*>(msw)[C::kMetaZp + j * 128 + r];
+                            const int32_t* asv = reinterpret_cast<const int32_t*>(msw) + C::kMetaAs + j * BN + c0 + ch * CW;
+#pragma unroll
+                            for (int q = 0; q < CW; ++q) v[q] = uint32_t(int32_t(v[q]) - zr * asv[q]);
+                        }
                         if constexpr (MODE == kDumpPartials) {
                             if (r < ti.rows) {
 #pragma unroll
-                                for (int q = 0; q < 16; ++q) {
-                                    const int64_t m = m0 + ch * 16 + q;
+                                for (int q = 0; q < CW; ++q) {
+                                    const int64_t m = m0 + ch * CW + q;
                                     if (m < p.M)
                                         p.partials[(int64_t(gc + j) * p.M + m) * p.partial_rows + ti.first + r] =
                                             int32_t(v[q]);
@@ -523,8 +598,8 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                             }
                         } else if constexpr (kPair) {
 #pragma unroll
-                            for (int q = 0; q < 16; q += 2) {
-                                const int jj = ch * 16 + q;
+                            for (int q = 0; q < CW; q += 2) {
+                                const int jj = ch * CW + q;
                                 // exact int -> f32 (|S| < 2^22), two lanes per FFMA2
                                 const uint64_t g2 = pk2(__int2float_rn(int32_t(v[q])), __int2float_rn(int32_t(v[q + 1])));
                                 if constexpr (MODE == kFastGroup) {
@@ -536,9 +611,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                             }
                         } else {
 #pragma unroll
-                            for (int q = 0; q < 16; ++q) {
+                            for (int q = 0; q < CW; ++q) {
                                 const float gs = __int2float_rn(int32_t(v[q]));  // exact: |S| < 2^22
-                                const int jj = ch * 16 + q;
+                                const int jj = ch * CW + q;
                                 if constexpr (MODE == kExactGroup) {
                                     // gemm.cpp:81 — out += gs * (s_a * s_w), no contraction
                                     acc[jj] = __fadd_rn(acc[jj], __fmul_rn(gs, __fmul_rn(sav[jj], sw)));
@@ -555,9 +630,13 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tempty[rt.idx]);
+                if (lane == 0) {
+                    ptx::mbar_arrive(&tempty[rt.idx]);
+                    ptx::mbar_arrive(&mempty[rm.idx]);
+                }
                 if (et == 0) trace_chunk(p, 4, n);
                 rt.next<NT>();
+                rm.next<C::NM>();
             }
             if (et == 0) trace(p, 4);
             if constexpr (kPair) {

@@ -22,7 +22,8 @@ enum GemmMode : int {
 //   codes  uint8 [G][Mpad][128]: byte (g, m, k) at g*Mpad*128 + m*128 +
 //          ((((k >> 4) ^ (m & 7)) << 4) | (k & 15))  — each (group, token-tile)
 //          is a ready UMMA K-major SWIZZLE_128B operand image;
-//   scales f32   [G][Mpad] (group-wise) or [Mpad] (per-token).
+//   scales f32   [G][Mpad] (group-wise) or [Mpad] (per-token);
+//   asum   int32 [G][Mpad] sum of each (group, token)'s codes.
 // Mpad = TB * BN (token tile BN); rows m >= M are zero. Ragged K groups are
 // zero-padded to 128.
 __host__ __device__ inline uint32_t eal_offset(uint32_t m, uint32_t k) {
@@ -51,6 +52,7 @@ struct GemmParams {
     // EAL activations (tensor-core kernel)
     const uint8_t* acts;    // [G][Mpad][128]
     const float* sa;        // [G][Mpad] (group-wise) or [Mpad] (per-token)
+    const int32_t* asum;    // [G][Mpad] per-(group, token) code sums (zero-point correction)
     int64_t Mpad;
     // row-major activations (SIMT debug kernel): scales sa_rm[g * sa_gstride + m]
     const float* sa_rm;
@@ -113,13 +115,16 @@ cudaError_t launch_mixed_gemm_simt(const GemmParams& p, const int8_t* codes, int
 cudaError_t launch_act_quant(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda,
                              int group, int f16_scales, int8_t* codes, int64_t ldc, float* scales,
                              int64_t lds, int32_t* err, bool pdl, cudaStream_t stream);
-// K1 (engine layout, EAL): group == 128 (group-wise) or K (per-token).
+// K1 (engine layout, EAL): group == 128 (group-wise) or K (per-token). Also
+// writes asum [G][Mpad] int32 = the sum of each (group, token)'s codes, the
+// zero-point correction term of the decode GEMM (sum a(c - z) = sum a c - z sum a).
 cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda, int group,
-                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* err, bool pdl,
+                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum, int32_t* err, bool pdl,
                                  cudaStream_t stream);
-// Row-major codes [M, ldc] + group-major scales [G, lds] (or [M]) -> EAL.
+// Row-major codes [M, ldc] + group-major scales [G, lds] (or [M]) -> EAL (+ asum).
 cudaError_t launch_repack_eal(const int8_t* codes, int64_t ldc, const float* scales, int64_t lds, int per_token,
-                              int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, cudaStream_t stream);
+                              int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum,
+                              cudaStream_t stream);
 cudaError_t launch_permute(const void* gathered, const int32_t* colmap, int world, int64_t shard_cols,
                            int64_t M, int64_t N, void* Y, int dtype, cudaStream_t stream);
 

@@ -22,7 +22,7 @@ raw = np.array(buf, dtype=np.float64)
 a = raw[:148*8].reshape(148, 8)
 base = a[:, 0][a[:, 0] > 0].min()
 a = np.where(a > 0, a - base, np.nan) / 1000.0
-names = ["start", "prod_pass1", "prod_after_gdw", "epi_first_tfull", "epi_seg_done", "epi_exit", "end"]
+names = ["start", "prod_all_issued", "prod_enter", "epi_first_tfull", "epi_unit_done", "epi_exit", "end", "prod_first_issue"]
 for i, nm in enumerate(names):
     col = a[:, i]
     print(f"{nm:16s} min {np.nanmin(col):7.2f} med {np.nanmedian(col):7.2f} max {np.nanmax(col):7.2f} us")
