@@ -78,12 +78,13 @@ void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
     if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1 || pl->bn > 32) return;
     int best = 1;
     if (ksplit >= 2) {
-        best = ksplit;
+        best = 1;
+        while (best * 2 <= ksplit) best *= 2;  // powers of two
     } else {
         // the largest S whose units still fit one round of the persistent grid
         // (a split reduction on the critical path of a multi-round CTA costs more
         // than the balance it buys)
-        for (int S = 2; S <= 8; ++S) {
+        for (int S = 2; S <= 8; S *= 2) {  // powers of two: the kernel decodes units with shifts
             if (L->G / S < 2) break;
             if (2 * S * L->tiles8 + S * L->tiles4 <= L->num_sms) best = S;
         }
@@ -92,7 +93,8 @@ void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
     // sub8 tiles stream twice the bytes of sub4 tiles: halve them too while
     // everything still fits one round
     const bool halve8 = best > 1 || 2 * L->tiles8 + L->tiles4 <= L->num_sms;
-    pl->S8 = halve8 ? std::min(2 * best, std::max(1, L->G)) : 1;
+    pl->S8 = halve8 ? 2 * best : 1;
+    while (pl->S8 > 1 && pl->S8 > L->G) pl->S8 >>= 1;
 }
 
 mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
@@ -159,6 +161,9 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dty
     p->ldy = L->world > 1 ? L->shard_cols : L->N;
     p->S4 = pl.S4;
     p->S8 = pl.S8;
+    auto lg2 = [](int x) { int l = 0; while ((1 << l) < x) ++l; return l; };
+    p->lgS4 = lg2(pl.S4);
+    p->lgS8 = lg2(pl.S8);
     p->units = pl.units;
     p->grid = pl.grid;
     p->rotate = pl.rotate ? 1 : 0;
@@ -526,6 +531,7 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
     }
     if (p.T8 + p.T4 == 0) return MQ_OK;
     p.S4 = p.S8 = 1;
+    p.lgS4 = p.lgS8 = 0;
     p.units = (p.T8 + p.T4) * pl.tb;
     p.grid = std::min(p.units, L->num_sms);
     p.partials = partials;

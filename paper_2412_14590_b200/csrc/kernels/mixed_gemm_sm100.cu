@@ -244,10 +244,13 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         U.wk = work_of(p, u);
         U.ti = tile_info(p, U.wk.tile);
         U.gps = U.ti.is8 ? C::GPS8 : GPS;
-        U.nch = (p.dbg & 8) ? 0 : (U.wk.g1 - U.wk.g0 + U.gps - 1) / U.gps;  // dbg&8: launch-floor probe
+        // gps is a power of two: shifts, not divisions (see work_of)
+        const int lgg = U.gps == 4 ? 2 : U.gps == 2 ? 1 : 0;
+        U.nch = (p.dbg & 8) ? 0 : (U.wk.g1 - U.wk.g0 + U.gps - 1) >> lgg;  // dbg&8: launch-floor probe
         // FAST modes start each unit at a different chunk of its K-slice so the
         // CTAs do not all read the same activation lines at the same time
-        U.rot = (p.rotate && U.nch > 1) ? int((uint32_t(u) * 7u) % uint32_t(U.nch)) : 0;
+        // (multiply-shift hash into [0, nch), no division)
+        U.rot = (p.rotate && U.nch > 1) ? int(((uint32_t(u) * 2654435761u >> 16) * uint32_t(U.nch)) >> 16) : 0;
         return U;
     };
     auto chunk_at = [&](const Unit& U, int i, int& gc, int& cg) {

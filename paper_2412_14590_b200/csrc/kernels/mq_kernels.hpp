@@ -61,7 +61,8 @@ struct GemmParams {
     void* Y;
     int32_t out_dtype;      // mq_dtype
     int64_t ldy;
-    int32_t S8, S4;         // K-slices per sub8 / sub4 item
+    int32_t S8, S4;         // K-slices per sub8 / sub4 item (powers of two)
+    int32_t lgS8, lgS4;     // log2 of S8 / S4: unit decoding uses shifts, not divisions
     int32_t units;          // work units (token block x tile x K-slice)
     int32_t grid;           // persistent CTAs (<= SMs): CTA b runs units b, b + grid, ...
     float* part;            // split-K partial tiles [units][BN][128] (slot = unit index)
@@ -79,22 +80,25 @@ struct GemmParams {
 struct Work {
     int tile, tb, g0, g1, S, sl, cta0, item;
 };
+// Decoding is on every role's critical path at kernel start (a chain of integer
+// divisions costs ~1 us per CTA), so slices are powers of two and decode uses
+// shifts; only token-tiled launches (TB > 1, prefill) divide.
 __host__ __device__ inline Work work_of(const GemmParams& p, int cta) {
     Work w;
-    const int per_tb = p.S8 * p.T8 + p.S4 * p.T4;
-    w.tb = cta / per_tb;
+    const int per_tb = (p.T8 << p.lgS8) + (p.T4 << p.lgS4);
+    w.tb = p.TB == 1 ? 0 : cta / per_tb;
     int u = cta - w.tb * per_tb;
-    if (u < p.S8 * p.T8) {
-        w.tile = u / p.S8, w.S = p.S8, w.sl = u - w.tile * p.S8;
+    if (u < (p.T8 << p.lgS8)) {
+        w.tile = u >> p.lgS8, w.S = p.S8, w.sl = u & (p.S8 - 1);
     } else {
-        u -= p.S8 * p.T8;
-        const int t = u / p.S4;
-        w.tile = p.T8 + t, w.S = p.S4, w.sl = u - t * p.S4;
+        u -= p.T8 << p.lgS8;
+        w.tile = p.T8 + (u >> p.lgS4), w.S = p.S4, w.sl = u & (p.S4 - 1);
     }
     w.cta0 = cta - w.sl;
     w.item = w.tb * (p.T8 + p.T4) + w.tile;
-    w.g0 = int((int64_t(w.sl) * p.G) / w.S);
-    w.g1 = int((int64_t(w.sl + 1) * p.G) / w.S);
+    const int lg = w.S == p.S8 ? p.lgS8 : p.lgS4;
+    w.g0 = (w.sl * p.G) >> lg;
+    w.g1 = ((w.sl + 1) * p.G) >> lg;
     return w;
 }
 
