@@ -47,6 +47,29 @@ __device__ __forceinline__ int8_t quant_one(float x, float s) {
     return static_cast<int8_t>(static_cast<int>(q));
 }
 
+// 4 consecutive activations (k .. k+3 of one row), zero past K
+template <int DT>
+__device__ __forceinline__ void load4(const void* A, int64_t base, int64_t k, int64_t K, bool vec, float (&x)[4]) {
+    if (vec && k + 3 < K) {
+        if constexpr (DT == 0) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(A) + base + k));
+            x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+        } else {
+            const uint2 v = __ldg(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(A) + base + k));
+            const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint16_t h = uint16_t(w[i >> 1] >> (16 * (i & 1)));
+                if constexpr (DT == 1) x[i] = __half2float(__ushort_as_half(h));
+                else x[i] = __bfloat162float(__ushort_as_bfloat16(h));
+            }
+        }
+        return;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = k + i < K ? load_act<DT>(A, base + k + i) : 0.0f;
+}
+
 // One warp per (token m, group g); group <= 4096.
 template <int DT>
 __global__ void act_quant_group_kernel(const void* __restrict__ A, int64_t M, int64_t K,
@@ -145,14 +168,12 @@ __global__ void act_quant_eal_group_kernel(const void* __restrict__ A, int64_t M
     float amax = 0.0f;
     bool finite = true;
     if (m < M) {
+        const bool vec = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & (DT == 0 ? 15 : 7)) == 0);
+        load4<DT>(A, m * lda, b + 4 * lane, K, vec, x);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int k = 4 * lane + i;
-            if (k < len) {
-                x[i] = load_act<DT>(A, m * lda + b + k);
-                finite &= isfinite(x[i]);
-                amax = fmaxf(amax, fabsf(x[i]));
-            }
+            finite &= isfinite(x[i]);
+            amax = fmaxf(amax, fabsf(x[i]));
         }
     }
     for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -180,28 +201,39 @@ __global__ void act_quant_eal_group_kernel(const void* __restrict__ A, int64_t M
 }
 
 // per-token (group == K): one CTA per token row m < Mpad
-template <int DT>
-__global__ void __launch_bounds__(256) act_quant_eal_row_kernel(const void* __restrict__ A, int64_t M, int64_t K,
-                                                                int64_t lda, int G, int64_t Mpad,
-                                                                uint8_t* __restrict__ acts, float* __restrict__ sa,
-                                                                int32_t* __restrict__ asum, int32_t* err) {
+// per-token (group == K): one 1024-thread CTA per token row m < Mpad. The row
+// is read ONCE into registers (4 values per thread per step, up to RV steps =
+// K <= 4096 * RV) with all loads in flight together — a grid-stride loop of
+// dependent loads here is latency-bound (~1 us per step).
+template <int DT, int RV>
+__global__ void __launch_bounds__(1024) act_quant_eal_row_kernel(const void* __restrict__ A, int64_t M, int64_t K,
+                                                                 int64_t lda, int G, int64_t Mpad,
+                                                                 uint8_t* __restrict__ acts, float* __restrict__ sa,
+                                                                 int32_t* __restrict__ asum, int32_t* err) {
     griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
     griddep_wait();    // the previous kernel's outputs (our inputs) are complete
-    __shared__ float red[8];
-    __shared__ int bad[8];
+    __shared__ float red[32];
+    __shared__ int bad[32];
     const int64_t m = blockIdx.x;
     const bool live = m < M;
+    const bool vec = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & (DT == 0 ? 15 : 7)) == 0);
+    float x[RV][4];
     float amax = 0.0f;
     bool finite = true;
-    if (live)
-        for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
-            const float x = load_act<DT>(A, m * lda + i);
-            finite &= isfinite(x);
-            amax = fmaxf(amax, fabsf(x));
+#pragma unroll
+    for (int v = 0; v < RV; ++v) {
+        const int64_t k = (int64_t(v) * blockDim.x + threadIdx.x) * 4;
+        if (live) load4<DT>(A, m * lda, k, K, vec, x[v]);
+        else x[v][0] = x[v][1] = x[v][2] = x[v][3] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            finite &= isfinite(x[v][i]);
+            amax = fmaxf(amax, fabsf(x[v][i]));
         }
+    }
     for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     const bool wfin = __all_sync(0xffffffffu, finite);
-    const int w = threadIdx.x >> 5;
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
         red[w] = amax;
         bad[w] = !wfin;
@@ -209,33 +241,30 @@ __global__ void __launch_bounds__(256) act_quant_eal_row_kernel(const void* __re
     __syncthreads();
     amax = red[0];
     int anybad = bad[0];
-    for (int i = 1; i < 8; ++i) {
+    for (int i = 1; i < nw; ++i) {
         amax = fmaxf(amax, red[i]);
         anybad |= bad[i];
     }
     if (live && anybad && threadIdx.x == 0 && err) atomicMin(err, static_cast<int32_t>(m));
     const float s = live ? act_scale(amax, 0) : 0.0f;
-    // 4 codes per thread-iteration, all G groups of this row; a warp covers one
-    // group per iteration (blockDim is a multiple of 32), so it also sums it
-    const int64_t qend = (int64_t(G) * 32 + blockDim.x - 1) / blockDim.x * blockDim.x;
-    for (int64_t q = threadIdx.x; q < qend; q += blockDim.x) {
-        const int g = static_cast<int>(q >> 5);
-        const int k0 = static_cast<int>(q & 31) * 4;
+    // a warp's 32 x 4 codes of step v are exactly one 128-wide group
+#pragma unroll
+    for (int v = 0; v < RV; ++v) {
+        const int64_t k = (int64_t(v) * blockDim.x + threadIdx.x) * 4;
+        const int g = static_cast<int>(k >> 7);
         uint32_t word = 0;
         int csum = 0;
-        if (live && g < G)
+        if (live)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int64_t k = int64_t(g) * 128 + k0 + i;
-                if (k < K) {
-                    const int8_t c = quant_one(load_act<DT>(A, m * lda + k), s);
+            for (int i = 0; i < 4; ++i)
+                if (k + i < K) {
+                    const int8_t c = quant_one(x[v][i], s);
                     csum += c;
                     word |= uint32_t(uint8_t(c)) << (8 * i);
                 }
-            }
         for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
         if (g < G) {
-            *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(k0))) = word;
+            *reinterpret_cast<uint32_t*>(acts + int64_t(g) * Mpad * 128 + eal_offset(uint32_t(m), uint32_t(k & 127))) = word;
             if ((threadIdx.x & 31) == 0) asum[int64_t(g) * Mpad + m] = csum;
         }
     }
@@ -303,11 +332,17 @@ cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t 
     const int G = static_cast<int>((K + 127) / 128);
     if (group >= K) {
         const dim3 grid(static_cast<unsigned>(Mpad));
+        const int64_t steps = (K + 4095) / 4096;  // 1024 threads x 4 values per step
+        if (steps > 8) return cudaErrorInvalidValue;  // K > 32768: not a Llama shape
+#define MQ_ROW(DT, RV) launch_ex(act_quant_eal_row_kernel<DT, RV>, grid, dim3(1024), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err)
+#define MQ_ROWS(DT) (steps <= 1 ? MQ_ROW(DT, 1) : steps <= 2 ? MQ_ROW(DT, 2) : steps <= 4 ? MQ_ROW(DT, 4) : MQ_ROW(DT, 8))
         switch (a_dtype) {
-            case 0: return launch_ex(act_quant_eal_row_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
-            case 1: return launch_ex(act_quant_eal_row_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
-            default: return launch_ex(act_quant_eal_row_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
+            case 0: return MQ_ROWS(0);
+            case 1: return MQ_ROWS(1);
+            default: return MQ_ROWS(2);
         }
+#undef MQ_ROWS
+#undef MQ_ROW
     }
     const int64_t warps = Mpad * G;
     const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));

@@ -91,7 +91,7 @@ struct TcCfg {
     static constexpr int NS = NS0 > MQ_NS_MAX ? MQ_NS_MAX : NS0;
     // epilogue warpgroups: two at decode too — one warp per SMSP would leave the
     // TMEM-load / rescale chain latency-bound
-    static constexpr int NE = (BN <= 32 || BN >= 128) ? 2 : 1;
+    static constexpr int NE = (BN == 16 || BN >= 128) ? 2 : 1;
     static constexpr int NC = BN <= 32 ? 2 : 1;  // converter warpgroups (decode is conversion-bound)
     static constexpr int BNE = BN / NE;          // tokens per epilogue warpgroup
     static constexpr int kEpiThread0 = 128 * (1 + NC);
@@ -664,12 +664,14 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 continue;
             }
             // split-K (decode token tiles only): publish this slice's partial tile
-            // [BN][128] (slot = unit), count arrivals; the last slice sums all S
-            // partials in slice order (deterministic) and scatters them
+            // [128][BN] (slot = unit; a thread's tokens are contiguous -> float4),
+            // count arrivals; the last slice sums all S partials in slice order
+            // (deterministic) and scatters them
             if constexpr (BN <= 32) {
-            float* mine = p.part + int64_t(u) * (BN * 128);
+            float4* mine = reinterpret_cast<float4*>(p.part + int64_t(u) * (BN * 128) + r * BN + c0);
 #pragma unroll
-            for (int j = 0; j < BNE; ++j) __stcg(mine + (c0 + j) * 128 + r, acc[j]);
+            for (int j = 0; j < BNE / 4; ++j)
+                __stcg(mine + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
             named_bar_sync(2, 128 * NE);
             if (et == 0) {
                 __threadfence();
@@ -683,22 +685,35 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
             if (last) {
                 __threadfence();
                 const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
-                const float* base = p.part + int64_t(wk.cta0) * (BN * 128) + c0 * 128 + r;
-                for (int j0 = 0; j0 < BNE; j0 += 2) {
-                    float t[2][16];
+                const float4* base = reinterpret_cast<const float4*>(p.part + int64_t(wk.cta0) * (BN * 128) + r * BN + c0);
+                constexpr int V = BNE / 4;              // float4s per slice
+                constexpr int SB = 32 / BNE;            // slices per batch: every load of a batch in flight
+                float sum[BNE];
+                for (int s0 = 0; s0 < wk.S; s0 += SB) {
+                    float4 t[SB][V];
 #pragma unroll
-                    for (int s2 = 0; s2 < 16; ++s2)
-                        if (s2 < wk.S)
+                    for (int s2 = 0; s2 < SB; ++s2)
+                        if (s0 + s2 < wk.S)
 #pragma unroll
-                            for (int q = 0; q < 2; ++q) t[q][s2] = __ldcg(base + int64_t(s2) * (BN * 128) + (j0 + q) * 128);
+                            for (int q = 0; q < V; ++q) t[s2][q] = __ldcg(base + int64_t(s0 + s2) * (BN * 32) + q);
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        float v = t[q][0];
+                    for (int s2 = 0; s2 < SB; ++s2) {
+                        if (s0 + s2 >= wk.S) break;
 #pragma unroll
-                        for (int s2 = 1; s2 < 16; ++s2)
-                            if (s2 < wk.S) v = __fadd_rn(v, t[q][s2]);
-                        const int64_t m = m0 + j0 + q;
-                        if (col >= 0 && m < p.M) {
+                        for (int q = 0; q < V; ++q) {
+                            const float tv[4] = {t[s2][q].x, t[s2][q].y, t[s2][q].z, t[s2][q].w};
+#pragma unroll
+                            for (int e4 = 0; e4 < 4; ++e4)
+                                sum[4 * q + e4] = (s0 + s2 == 0) ? tv[e4] : __fadd_rn(sum[4 * q + e4], tv[e4]);
+                        }
+                    }
+                }
+                if (col >= 0) {
+#pragma unroll
+                    for (int j = 0; j < BNE; ++j) {
+                        const int64_t m = m0 + j;
+                        if (m < p.M) {
+                            float v = sum[j];
                             if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
                             store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
                         }
