@@ -113,8 +113,17 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Development instrumentation (globaltimer / clock64 traces, MQ_DBG stage
+// bypasses) is compiled only with -DMQ_DEV (tools/ builds it beside the
+// product library): every check sits on the per-chunk hot path.
+#ifdef MQ_DEV
+constexpr bool kDev = true;
+#else
+constexpr bool kDev = false;
+#endif
+__device__ __forceinline__ int dbg_bits(const GemmParams& p) { return kDev ? p.dbg : 0; }
 __device__ __forceinline__ void trace(const GemmParams& p, int ev) {
-    if (p.trace) {
+    if (kDev && p.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
         p.trace[blockIdx.x * 8 + ev] = t;
@@ -122,7 +131,7 @@ __device__ __forceinline__ void trace(const GemmParams& p, int ev) {
 }
 // per-chunk event trace of one CTA (MQ_DBG & 64, CTA = MQ_DBG >> 8), in SM cycles
 __device__ __forceinline__ void trace_chunk(const GemmParams& p, int ev, int n) {
-    if (p.trace && (p.dbg & 64) && int(blockIdx.x) == (p.dbg >> 8) && n < 64)
+    if (kDev && p.trace && (p.dbg & 64) && int(blockIdx.x) == (p.dbg >> 8) && n < 64)
         p.trace[148 * 8 + ev * 64 + n] = clock64();
 }
 
@@ -246,7 +255,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         U.gps = U.ti.is8 ? C::GPS8 : GPS;
         // gps is a power of two: shifts, not divisions (see work_of)
         const int lgg = U.gps == 4 ? 2 : U.gps == 2 ? 1 : 0;
-        U.nch = (p.dbg & 8) ? 0 : (U.wk.g1 - U.wk.g0 + U.gps - 1) >> lgg;  // dbg&8: launch-floor probe
+        U.nch = (dbg_bits(p) & 8) ? 0 : (U.wk.g1 - U.wk.g0 + U.gps - 1) >> lgg;  // dbg&8: launch-floor probe
         // FAST modes start each unit at a different chunk of its K-slice so the
         // CTAs do not all read the same activation lines at the same time
         // (multiply-shift hash into [0, nch), no division)
@@ -333,7 +342,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         }
     } else if (warp == 1) {
         // ======================= TMEM allocation + MMA issuer ==================
-        if (!(p.dbg & 16)) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);  // dbg&16 (with &8): launch-floor probe
+        if (!(dbg_bits(p) & 16)) ptx::tmem_alloc<C::kTmemCols>(tmem_holder);  // dbg&16 (with &8): launch-floor probe
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(tmem_ready);
@@ -359,7 +368,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 const uint32_t st = ptx::smem_u32(stage(rs.idx));
                 const uint32_t xs = ptx::smem_u32(xstage(rx.idx));
                 if (elect_one()) {
-                    if (!(p.dbg & 4)) {
+                    if (!(dbg_bits(p) & 4)) {
                         for (int j = 0; j < cg; ++j) {
                             const uint32_t d_tmem = tmem_base + uint32_t((rt.idx * GPS + j) * BN);
                             const uint32_t b_addr = xs + j * (BN * 128);
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                                 }
                             }
                         }
-                        if (!(p.dbg & 2)) ptx::tmem_st32(tmem_row + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32), v);
+                        if (!(dbg_bits(p) & 2)) ptx::tmem_st32(tmem_row + C::kACol0 + uint32_t((ra.idx * GPS + j) * 32), v);
                     }
                     msw[j * 128 + r] = swv[jj];
                     if constexpr (C::kZpEpi) reinterpret_cast<int32_t*>(msw)[C::kMetaZp + j * 128 + r] = int32_t(kk[jj]);
@@ -536,7 +545,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                     // decode: two groups' sums in flight per wait (register budget)
 #pragma unroll
                     for (int j0 = 0; j0 < GPS; j0 += 2) {
-                        if (j0 >= cg || (p.dbg & 1)) break;
+                        if (j0 >= cg || (dbg_bits(p) & 1)) break;
                         uint32_t v[2][BNE];
 #pragma unroll
                         for (int h = 0; h < 2; ++h)
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                     constexpr int CW = BNE < 16 ? BNE : 16;  // TMEM columns per load
 #pragma unroll
                     for (int ch = 0; ch < BNE / CW; ++ch) {
-                        if (p.dbg & 1) break;
+                        if (dbg_bits(p) & 1) break;
                         uint32_t v[CW];
                         if constexpr (CW == 16) ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * 16, v);
                         else ptx::tmem_ld8(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * CW, v);
@@ -728,7 +737,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) trace(p, 6);
-    if (warp == 1 && !(p.dbg & 16)) {
+    if (warp == 1 && !(dbg_bits(p) & 16)) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::kTmemCols>(*reinterpret_cast<volatile uint32_t*>(tmem_holder));
     }
