@@ -116,7 +116,7 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     pl->Mpad = int64_t(pl->tb) * pl->bn;
     pl->mode = o->mode == MQ_EXACT ? (pl->per_token ? kExactToken : kExactGroup) : (pl->per_token ? kFastToken : kFastGroup);
     pl->pdl = o->no_pdl == 0;
-    pl->rotate = o->mode == MQ_FAST && pl->tb == 1;  // decode: stagger the CTAs' activation reads
+    pl->rotate = o->mode == MQ_FAST;  // stagger the CTAs' (shared, L2-resident) activation reads
     choose_split(L, pl, o->ksplit);
     pl->units = static_cast<int>((int64_t(pl->S8) * L->tiles8 + int64_t(pl->S4) * L->tiles4) * pl->tb);
     pl->grid = std::min(pl->units, L->num_sms);

@@ -63,7 +63,9 @@ struct TcCfg {
     static constexpr int kOffSa = GPS * BN * 128;
     static constexpr int kOffAs = kOffSa + GPS * BN * 4;
     static constexpr int kXStageBytes = ((kOffAs + (kZpEpi ? GPS * BN * 4 : 0)) + 1023) / 1024 * 1024;
-    static constexpr int NX = 3;  // activation stages
+    // activation stages: a prefill tile needs a fresh 16 KB activation tile per
+    // group (from L2), so its ring is as deep as the weight ring
+    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? 6 : 3;
     // TMEM rings (512 columns): NT accumulator chunk slots of GPS x BN int32
     // columns, NA A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
