@@ -205,6 +205,8 @@ typedef struct {
     int32_t token_tile;  /* 0 = auto; else 16/32/64/128 */
     int32_t gemm_impl;   /* 0 = tcgen05 (product); 1 = SIMT debug kernel */
     int32_t no_pdl;      /* 1 = plain launches (default: programmatic dependent launch) */
+    int32_t schedule;    /* MQ_FAST token-tiled launches: 0 = auto, 1 = unit rounds, 2 = stream-K
+                            (equal work per SM; each cut item summed head + tail) where it applies */
 } mq_exec_opts;
 
 /* Bytes of scratch a forward needs: split-K arrival counters + partial tiles

@@ -51,7 +51,7 @@ class mq_layer_info(C.Structure):
 
 class mq_exec_opts(C.Structure):
     _fields_ = [("mode", I32), ("act_group", I32), ("ksplit", I32), ("token_tile", I32), ("gemm_impl", I32),
-                ("no_pdl", I32)]
+                ("no_pdl", I32), ("schedule", I32)]
 
 
 # name -> (restype, argtypes); mirrors capi.h one to one.

@@ -66,8 +66,54 @@ int auto_token_tile(int64_t M) {
 struct Plan {
     int bn, tb, mode, per_token, S4, S8, units, grid;
     int64_t Mpad;
-    bool pdl, rotate;
+    bool pdl, rotate, sk;
+    std::vector<uint32_t> skb;  // stream-K boundaries [grid + 1]
 };
+
+// Stream-K plan (mq_kernels.hpp): equal cost per CTA over the item sequence,
+// boundaries rounded down to the tile's chunk size. Used by FAST token-tiled
+// launches when the unit schedule's last round would leave CTAs idle for
+// longer than a cut item costs; every CTA gets >= 2 items of work, so an item
+// is cut at most once (head + tail, sk_piece_done).
+bool stream_k_pays(const mq_layer_s* L, const Plan* pl, bool force) {
+    const int64_t G = L->G, items = int64_t(pl->tb) * (L->tiles8 + L->tiles4);
+    const int grid = std::min<int>(L->num_sms, kSkMax);
+    const double per_cta = double(items * G) / grid;  // groups (prefill: a sub8 group costs as a sub4 one)
+    if (per_cta < 2.0 * G) return false;
+    if (force) return true;
+    const int64_t rounds = (items + grid - 1) / grid;
+    const double cut_cost = 16.0;  // measured: publish + join + tail of a cut item ~ 16 groups
+    return per_cta + cut_cost < double(rounds * G);
+}
+
+void plan_stream_k(const mq_layer_s* L, Plan* pl) {
+    const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4, T = T8 + T4;
+    const int64_t c8 = pl->bn <= 32 ? 2 : 1;
+    const int gps = gemm_gps(pl->bn), gps8 = gps / 2 > 0 ? gps / 2 : 1;
+    const int64_t ctb = T8 * G * c8 + T4 * G, total = ctb * pl->tb;
+    const int64_t chunks = (T8 * ((G + gps8 - 1) / gps8) + T4 * ((G + gps - 1) / gps)) * pl->tb;
+    const int grid = static_cast<int>(std::min<int64_t>({L->num_sms, kSkMax, chunks}));
+    pl->skb.assign(size_t(grid) + 1, 0);
+    for (int b = 0; b < grid; ++b) {
+        const int64_t x = total * b / grid;
+        const int64_t tb = x / ctb, rr = x - tb * ctb;
+        int64_t t, g;
+        if (rr < T8 * G * c8) {
+            t = rr / (G * c8);
+            g = (rr - t * G * c8) / c8;
+            g = g / gps8 * gps8;
+        } else {
+            const int64_t r4 = rr - T8 * G * c8;
+            t = T8 + r4 / G;
+            g = r4 - (t - T8) * G;
+            g = g / gps * gps;
+        }
+        pl->skb[b] = static_cast<uint32_t>(((tb * T + t) << 8) | g);
+    }
+    pl->skb[grid] = static_cast<uint32_t>((int64_t(pl->tb) * T) << 8);
+    pl->grid = grid;
+    pl->sk = true;
+}
 
 // K-slices per item (mq_kernels.hpp schedule). Exact mode keeps the
 // reference's ascending group order per output, so it never splits; token-
@@ -120,6 +166,13 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     choose_split(L, pl, o->ksplit);
     pl->units = static_cast<int>((int64_t(pl->S8) * L->tiles8 + int64_t(pl->S4) * L->tiles4) * pl->tb);
     pl->grid = std::min(pl->units, L->num_sms);
+    pl->sk = false;
+    // stream-K when the unit schedule's last round would leave CTAs idle
+    if (o->schedule < 0 || o->schedule > 2) return fail(MQ_USAGE, "schedule must be 0 (auto), 1 (units) or 2 (stream-K)");
+    const int64_t items = int64_t(pl->tb) * (L->tiles8 + L->tiles4);
+    if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn >= 64 && L->G < 256 && items * 256 < (int64_t(1) << 32) &&
+        o->schedule != 1 && stream_k_pays(L, pl, o->schedule == 2))
+        plan_stream_k(L, pl);
     return MQ_OK;
 }
 
@@ -135,7 +188,8 @@ EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
     const size_t items = size_t(pl.tb) * size_t(L->tiles8 + L->tiles4);
     w.off_part = al(items * 4);
     const bool split = pl.S4 > 1 || pl.S8 > 1;
-    w.off_acts = w.off_part + (split ? al(size_t(pl.units) * 128 * size_t(pl.bn) * 4) : 0);
+    const size_t slots = pl.sk ? size_t(pl.grid) + 1 : split ? size_t(pl.units) : 0;
+    w.off_acts = w.off_part + al(slots * 128 * size_t(pl.bn) * 4);
     w.off_sa = w.off_acts + al(size_t(L->G) * size_t(pl.Mpad) * 128);
     const int64_t Ga = pl.per_token ? 1 : L->G;
     w.off_asum = w.off_sa + al(size_t(Ga) * size_t(pl.Mpad) * 4);
@@ -167,6 +221,9 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dty
     p->units = pl.units;
     p->grid = pl.grid;
     p->rotate = pl.rotate ? 1 : 0;
+    p->T = static_cast<int32_t>(L->tiles8 + L->tiles4);
+    p->sk = pl.sk ? 1 : 0;
+    if (pl.sk) std::copy(pl.skb.begin(), pl.skb.end(), p->skb);
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
     static const int dbg = [] {
         const char* e = std::getenv("MQ_DBG");

@@ -182,6 +182,61 @@ __device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& l
     hi = (((w >> 4) & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
 }
 
+// Stream-K split piece epilogue. The plan gives every CTA at least two items
+// of work, so an item is cut at most once: its HEAD (groups [0, g)) is the last
+// piece of CTA b and its TAIL (groups [g, G)) the first piece of CTA b + 1,
+// which finishes it long before CTA b reaches the head. The tail publishes its
+// partial tile to slot b + 1 ([slot][BN/4][128] float4: a warp's stores are 512
+// contiguous bytes) and raises the item's flag; the head waits for the flag
+// (co-resident persistent grid: no deadlock), adds the tail's partial to its
+// own (head + tail: one rounding, order-independent, deterministic) and
+// returns true so the caller scatters the sum. Returns false for a tail.
+template <int BN, int BNE, int NE>
+__device__ __noinline__ bool sk_piece_done(const GemmParams& p, const Work& wk, float* acc, int r, int c0, int et) {
+    constexpr int V = BNE / 4;
+    float4* part4 = reinterpret_cast<float4*>(p.part);
+    if (wk.g0 > 0) {  // tail
+        float4* mine = part4 + (int64_t(blockIdx.x) * (BN / 4) + c0 / 4) * 128 + r;
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            __stcg(mine + j * 128, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
+        named_bar_sync(2, 128 * NE);
+        if (et == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + wk.item), "r"(1u) : "memory");
+        }
+        return false;
+    }
+    // head
+    if (et == 0) {
+        uint32_t f = 0;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(p.cnt + wk.item) : "memory");
+            if (f) break;
+            __nanosleep(64);
+        }
+        p.cnt[wk.item] = 0u;  // re-arm for the next launch
+    }
+    named_bar_sync(2, 128 * NE);
+    __threadfence();
+    const float4* src = part4 + (int64_t(blockIdx.x + 1) * (BN / 4) + c0 / 4) * 128 + r;
+    constexpr int VB = V < 8 ? V : 8;  // float4 loads in flight per batch
+#pragma unroll
+    for (int j0 = 0; j0 < V; j0 += VB) {
+        float4 t[VB];
+#pragma unroll
+        for (int q = 0; q < VB; ++q) t[q] = __ldcg(src + (j0 + q) * 128);
+#pragma unroll
+        for (int q = 0; q < VB; ++q) {
+            acc[4 * (j0 + q) + 0] = __fadd_rn(acc[4 * (j0 + q) + 0], t[q].x);
+            acc[4 * (j0 + q) + 1] = __fadd_rn(acc[4 * (j0 + q) + 1], t[q].y);
+            acc[4 * (j0 + q) + 2] = __fadd_rn(acc[4 * (j0 + q) + 2], t[q].z);
+            acc[4 * (j0 + q) + 3] = __fadd_rn(acc[4 * (j0 + q) + 3], t[q].w);
+        }
+    }
+    return true;
+}
+
 template <int BN, int MODE>
 __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(const __grid_constant__ GemmParams p) {
     using C = TcCfg<BN>;
@@ -248,11 +303,12 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     struct Unit {
         Work wk;
         TileInfo ti;
-        int gps, nch, rot;
+        int gps, nch, rot, key;
     };
-    auto unit_at = [&](int u) {
+    auto unit_of = [&](const Work& w, int u) {
         Unit U;
-        U.wk = work_of(p, u);
+        U.wk = w;
+        U.key = u;
         U.ti = tile_info(p, U.wk.tile);
         U.gps = U.ti.is8 ? C::GPS8 : GPS;
         // gps is a power of two: shifts, not divisions (see work_of)
@@ -264,13 +320,39 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         U.rot = (p.rotate && U.nch > 1) ? int(((uint32_t(u) * 2654435761u >> 16) * uint32_t(U.nch)) >> 16) : 0;
         return U;
     };
+    const int u0 = blockIdx.x, ustep = gridDim.x;
+    // k-th piece of work of this CTA. Unit schedule: units u0, u0 + grid, ...
+    // Stream-K schedule (p.sk): the CTA's contiguous range [skb[b], skb[b+1])
+    // of (item, group) positions, cut into one piece per item it touches; a
+    // piece that is not a whole item is "split" (S = 2; see sk_piece_done).
+    auto piece = [&](int k, Unit& U) -> bool {
+        if (!p.sk) {
+            const int u = u0 + k * ustep;
+            if (u >= p.units) return false;
+            U = unit_of(work_of(p, u), u);
+            return true;
+        }
+        const uint32_t a = p.skb[blockIdx.x], e = p.skb[blockIdx.x + 1];
+        const int it = int(a >> 8) + k, ie = int(e >> 8);
+        if (it > ie || (it == ie && (e & 255u) == 0u)) return false;
+        Work w;
+        w.item = it;
+        w.tb = p.TB == 1 ? 0 : it / p.T;
+        w.tile = it - w.tb * p.T;
+        w.g0 = k == 0 ? int(a & 255u) : 0;
+        w.g1 = it == ie ? int(e & 255u) : p.G;
+        w.S = (w.g0 == 0 && w.g1 == p.G) ? 1 : 2;
+        w.sl = 0;
+        w.cta0 = 0;
+        U = unit_of(w, it);
+        return true;
+    };
     auto chunk_at = [&](const Unit& U, int i, int& gc, int& cg) {
         int c = i + U.rot;
         if (c >= U.nch) c -= U.nch;
         gc = U.wk.g0 + c * U.gps;
         cg = (U.wk.g1 - gc) < U.gps ? (U.wk.g1 - gc) : U.gps;
     };
-    const int u0 = blockIdx.x, ustep = gridDim.x;
 
     if (warp == 0) {
         // ============================== producer ==============================
@@ -280,8 +362,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         // (griddepcontrol), so under PDL the first NS stages fill while it runs
         Ring rr;
         int n = 0;  // chunk counter across units
-        for (int u = u0; u < p.units; u += ustep) {
-            const Unit U = unit_at(u);
+        for (int pk = 0;; ++pk) {
+            Unit U;
+            if (!piece(pk, U)) break;
             for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
@@ -306,13 +389,16 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         const bool contig = p.Mpad == BN;  // one token tile: a chunk's act tiles are contiguous
         griddep_wait();  // K1's output
         Ring rx;
-        for (int u = u0; u < p.units; u += ustep) {
-            const Unit U = unit_at(u);
-            for (int i = 0; i < U.nch; ++i) {
+        int n = 0;
+        for (int pk = 0;; ++pk) {
+            Unit U;
+            if (!piece(pk, U)) break;
+            for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
                 uint8_t* xs = xstage(rx.idx);
                 ptx::mbar_wait(&xempty[rx.idx], rx.ph ^ 1u);
+                if (lane == 0) trace_chunk(p, 10, n);
                 if (elect_one()) {
                     ptx::mbar_arrive_expect_tx(&xfull[rx.idx], uint32_t(cg * BN * 128 + (kSa ? cg * BN * 4 : 0) +
                                                                         (C::kZpEpi ? cg * BN * 4 : 0)));
@@ -354,16 +440,20 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         const uint32_t idesc8 = p.idesc8 | ((uint32_t(BN) >> 3) << 17);
         Ring rs, ra, rt, rx;
         int n = 0;
-        for (int u = u0; u < p.units; u += ustep) {
-            const Unit U = unit_at(u);
+        for (int pk = 0;; ++pk) {
+            Unit U;
+            if (!piece(pk, U)) break;
             for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
                 // the weight stage is read here only for sub8 chunks (A in SMEM);
                 // sub4 weight stages are released by the converter alone
                 if (U.ti.is8) ptx::mbar_wait(&full[rs.idx], rs.ph);
+                if (lane == 0) trace_chunk(p, 7, n);
                 ptx::mbar_wait(&xfull[rx.idx], rx.ph);
+                if (lane == 0) trace_chunk(p, 8, n);
                 ptx::mbar_wait(&afull[ra.idx], ra.ph);
+                if (lane == 0) trace_chunk(p, 9, n);
                 ptx::mbar_wait(&tempty[rt.idx], rt.ph ^ 1u);
                 ptx::tc_fence_after();
                 if (lane == 0) trace_chunk(p, 1, n);
@@ -411,8 +501,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         const uint32_t tmem_row = *reinterpret_cast<volatile uint32_t*>(tmem_holder) + (uint32_t((warp & 3) * 32) << 16);
         Ring rs, ra, rm, rx;
         int n = 0;
-        for (int u = u0; u < p.units; u += ustep) {
-            const Unit U = unit_at(u);
+        for (int pk = 0;; ++pk) {
+            Unit U;
+            if (!piece(pk, U)) break;
             for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
@@ -515,8 +606,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         griddep_wait();  // scales / output of this launch are ours now
         Ring rt, rm;
         int n = 0;
-        for (int u = u0; u < p.units; u += ustep) {
-            const Unit U = unit_at(u);
+        for (int pk = 0;; ++pk) {
+            Unit U;
+            if (!piece(pk, U)) break;
             const Work& wk = U.wk;
             const TileInfo& ti = U.ti;
             const int64_t m0 = int64_t(wk.tb) * BN + c0;  // first token of this warpgroup
@@ -542,6 +634,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 ptx::mbar_wait(&tfull[rt.idx], rt.ph);
                 ptx::tc_fence_after();
                 if (n == 0 && et == 0) trace(p, 3);
+                if (et == 0) trace_chunk(p, 13, n);
                 const float* msw = meta + rm.idx * (C::kMetaSlot / 4);
                 if constexpr (kPair && (BNE == 16 || BNE == 8)) {
                     // decode: two groups' sums in flight per wait (register budget)
@@ -658,9 +751,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 for (int j = 0; j < BNE / 2; ++j) upk2(acc2[j], acc[2 * j], acc[2 * j + 1]);
             }
             if (MODE == kDumpPartials || U.nch == 0) continue;
-            if (wk.S == 1) {
-                // whole-K tile: scatter straight to the original output columns
-                const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
+            // scatter this thread's row to its original output column
+            const int col = (r < ti.rows && !(dbg_bits(p) & 128)) ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
+            auto store_acc = [&]() {
                 if (col >= 0) {
 #pragma unroll
                     for (int j = 0; j < BNE; ++j) {
@@ -672,14 +765,33 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                         }
                     }
                 }
+            };
+            if (wk.S == 1) {  // whole-K tile
+                if (et == 0) trace_chunk(p, 11, n);
+                store_acc();
+                if (et == 0) trace_chunk(p, 12, n);
                 continue;
+            }
+            if constexpr (MODE == kFastGroup || MODE == kFastToken) {
+            if (p.sk) {
+                // stream-K split piece (out of line: its registers would push
+                // the accumulation loop into spills)
+                float tmp[BNE];
+#pragma unroll
+                for (int j = 0; j < BNE; ++j) tmp[j] = acc[j];
+                if (!sk_piece_done<BN, BNE, NE>(p, wk, tmp, r, c0, et)) continue;
+#pragma unroll
+                for (int j = 0; j < BNE; ++j) acc[j] = tmp[j];
+                store_acc();
+                continue;
+            }
             }
             // split-K (decode token tiles only): publish this slice's partial tile
             // [128][BN] (slot = unit; a thread's tokens are contiguous -> float4),
             // count arrivals; the last slice sums all S partials in slice order
             // (deterministic) and scatters them
             if constexpr (BN <= 32) {
-            float4* mine = reinterpret_cast<float4*>(p.part + int64_t(u) * (BN * 128) + r * BN + c0);
+            float4* mine = reinterpret_cast<float4*>(p.part + int64_t(U.key) * (BN * 128) + r * BN + c0);
 #pragma unroll
             for (int j = 0; j < BNE / 4; ++j)
                 __stcg(mine + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));

@@ -41,6 +41,14 @@ __host__ __device__ inline uint32_t eal_offset(uint32_t m, uint32_t k) {
 // tile to its own workspace slot and bumps the item's counter; the LAST slice
 // to arrive sums the S partials in slice order (deterministic) and scatters
 // the result, then re-arms the counter.
+// Stream-K schedule (FAST modes, host-planned, GemmParams::sk): the work is
+// the sequence of ITEMS (token block, tile) x G groups, in cost units (a sub8
+// group costs c8 = 2 at decode, where bytes rule, and 1 when token-tiled);
+// CTA b runs positions [skb[b], skb[b+1]) packed as item << 8 | group, cut at
+// chunk boundaries. Items cut between CTAs are reduced by the piece that
+// completes their G groups (arrival counter counts groups).
+constexpr int kSkMax = 160;  // >= SMs of the device
+
 struct GemmParams {
     int32_t T8, T4;         // 128-row tiles of sub8 / sub4
     int64_t n8, n4;         // rows of sub8 / sub4
@@ -71,6 +79,9 @@ struct GemmParams {
     uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int32_t* partials;      // dump mode
     int32_t partial_rows;
+    int32_t sk;             // 1: stream-K schedule (skb), 0: unit schedule (units/S8/S4)
+    int32_t T;              // T8 + T4
+    uint32_t skb[kSkMax + 1];  // stream-K CTA boundaries (item << 8 | group)
     int32_t dbg;            // development: pipeline-stage bypass bits (MQ_DBG env), 0 in production
     unsigned long long* trace;  // development: per-CTA globaltimer stamps [P][8] (MQ_DBG & 32)
 };

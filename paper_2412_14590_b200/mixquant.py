@@ -246,8 +246,8 @@ def _stream(stream):
 
 
 def exec_opts(mode: int = capi.MQ_EXACT, act_group: int = 0, ksplit: int = 0, token_tile: int = 0,
-              gemm_impl: int = 0, pdl: bool = True) -> capi.mq_exec_opts:
-    return capi.mq_exec_opts(mode, act_group, ksplit, token_tile, gemm_impl, 0 if pdl else 1)
+              gemm_impl: int = 0, pdl: bool = True, schedule: int = 0) -> capi.mq_exec_opts:
+    return capi.mq_exec_opts(mode, act_group, ksplit, token_tile, gemm_impl, 0 if pdl else 1, schedule)
 
 
 class DeviceLayer:

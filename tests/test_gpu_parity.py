@@ -137,6 +137,22 @@ def test_fast_mode_within_tolerance(cuda, m):
     assert _rel(Y, ref) <= TOL
 
 
+@pytest.mark.parametrize("m,tt,sched", [(576, 64, 2), (1100, 128, 2), (1100, 128, 1), (1100, 128, 0)])
+def test_fast_mode_stream_k(cuda, m, tt, sched):
+    """Stream-K schedule (cut items summed head + tail) vs unit rounds: both
+    within tolerance of the oracle, and bit-reproducible run to run."""
+    import torch
+    L, A = _layer(m, 4096, 1024, 0.1, seed=21)
+    dl = mq.DeviceLayer(L)
+    o = mq.exec_opts(capi.MQ_FAST, 128, token_tile=tt, schedule=sched)
+    dA = torch.from_numpy(A).to(cuda)
+    Y = dl.forward(dA, opts=o).cpu().numpy()
+    ref, _, _ = O.mixed_linear(_oracle_layer(L), A)
+    assert _rel(Y, ref) <= TOL
+    for _ in range(2):
+        assert np.array_equal(dl.forward(dA, opts=o).cpu().numpy(), Y)
+
+
 @pytest.mark.parametrize("m", [1, 16, 100])
 def test_per_token_fast_mode_within_tolerance(cuda, m):
     import torch

@@ -29,8 +29,8 @@ for i, nm in enumerate(names):
 
 ch = raw[148*8:].reshape(16, 64)
 b = min(v for v in ch[:8].reshape(-1) if v > 0)
-print("CTA chunk timeline (kcycles): issue / mma_start / mma_commit / conv_done / epi_done / conv_full / conv_waits")
-for n in range(40):
-    row = ch[:7, n]
-    if row[1] == 0: continue
+print("CTA chunk timeline (kcycles): issue / mma_start / mma_commit / conv_done / epi_done / conv_full / conv_waits / mma_wfull / mma_wx / mma_wa / xprod_issue / store_begin / store_end / epi_start")
+for n in range(int(os.environ.get('NCH', '40'))):
+    row = ch[:14, n]
+    if row[1] == 0 and row[11] == 0: continue
     print(n, " ".join(f"{(v-b)/1000:7.2f}" if v > 0 else "    -  " for v in row))

@@ -33,7 +33,7 @@ def bench(n, k, m, mode, act_group=128, iters=50, reps=8, token_tile=0, ksplit=0
     print(f"N={n} K={k} M={m} mode={mode} ag={act_group}: {us:.2f} us  {byts/us/1e3:.0f} GB/s  {2*m*n*k/us/1e6:.1f} TOPS", flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "prefill"):
     for m in (1, 16, 64, 128, 256, 512):
         bench(4096, 4096, m, capi.MQ_FAST)
     for m in (16, 512):
@@ -42,3 +42,11 @@ if __name__ == "__main__":
     for m in (16, 512):
         bench(14336, 4096, m, capi.MQ_FAST, reps=4)
         bench(28672, 8192, m, capi.MQ_FAST, reps=2)
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "prefill":
+    for m in (256, 512, 1024, 2048):
+        bench(14336, 4096, m, capi.MQ_FAST, reps=4, iters=20)
+    bench(4096, 4096, 1024, capi.MQ_FAST, iters=20)
+    bench(4096, 14336, 1024, capi.MQ_FAST, reps=4, iters=20)
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "decode":
+    for (n, k) in ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336), (28672, 8192), (8192, 28672)):
+        bench(n, k, 16, capi.MQ_FAST, reps=4)

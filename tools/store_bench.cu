@@ -1,0 +1,64 @@
+// Microbenchmark: the K2 unit-end output scatter (thread = tile row, loop over
+// tokens, Y[m][colmap[r]]) vs contiguous / staged alternatives.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include <random>
+#include <cuda_fp16.h>
+
+template <int MODE>
+__global__ void __launch_bounds__(256) scatter(__half* Y, const int* colmap, int N, int M, int tiles, int units) {
+    const int r = threadIdx.x & 127, e = threadIdx.x >> 7;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tile = u % tiles, tb = u / tiles;
+        int col = MODE == 1 ? tile * 128 + r : colmap[tile * 128 + r];
+        if (col >= N) col = -1;
+        float acc[64];
+#pragma unroll
+        for (int j = 0; j < 64; ++j) acc[j] = float(j + r);
+        if (col >= 0) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+                const long m = long(tb) * 128 + e * 64 + j;
+                if (m < M) Y[m * N + col] = __float2half_rn(acc[j]);
+            }
+        }
+    }
+}
+
+int main() {
+    const int N = 14336, M = 512, tiles = N / 128, units = tiles * (M / 128);
+    std::vector<int> cm(N);
+    // realistic partition: 10% of columns (random) to "sub8", rest to "sub4", tiles in partition order
+    std::mt19937 g(1);
+    std::vector<int> idx(N);
+    for (int i = 0; i < N; ++i) idx[i] = i;
+    std::shuffle(idx.begin(), idx.end(), g);
+    std::vector<int> s8(idx.begin(), idx.begin() + N / 10), s4(idx.begin() + N / 10, idx.end());
+    std::sort(s8.begin(), s8.end());
+    std::sort(s4.begin(), s4.end());
+    int k = 0;
+    for (int c : s8) cm[k++] = c;
+    for (int c : s4) cm[k++] = c;
+    int* dcm; __half* Y; char* flush;
+    cudaMalloc(&dcm, N * 4); cudaMalloc(&Y, size_t(M) * N * 2); cudaMalloc(&flush, 256 << 20);
+    cudaMemcpy(dcm, cm.data(), N * 4, cudaMemcpyHostToDevice);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int mode = 0; mode < 4; ++mode) {
+        for (int rep = 0; rep < 2; ++rep) {
+            if (mode == 2) cudaMemset(flush, rep, 256 << 20);      // Y evicted from L2
+            if (mode == 3) cudaMemset(Y, 0, size_t(M) * N * 2);    // Y warm in L2
+            cudaEventRecord(a);
+            if (mode == 1) scatter<1><<<148, 256>>>(Y, dcm, N, M, tiles, units);
+            else scatter<0><<<148, 256>>>(Y, dcm, N, M, tiles, units);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            if (rep) printf("mode %d (%s): %.2f us  %.2f GB/s\n", mode,
+                            mode == 0 ? "scatter, back-to-back" : mode == 1 ? "contiguous" : mode == 2 ? "scatter, Y cold" : "scatter, Y warm",
+                            ms * 1e3, M * double(N) * 2 / ms / 1e6);
+        }
+    }
+    printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+}
