@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -33,6 +34,7 @@ struct mq_layer_s {
     int64_t shard_cols = 0;
     int w8_mode = MQ_W8_REFERENCE;
     int64_t tiles8 = 0, tiles4 = 0;
+    int split4 = 1, split8 = 1;         // decode K-split chosen once at create (choose_split)
     uint8_t* d_wq = nullptr;
     int32_t* d_colmap = nullptr;
     int64_t bytes_wq = 0, stream_bytes = 0;
@@ -117,30 +119,52 @@ void plan_stream_k(const mq_layer_s* L, Plan* pl) {
 
 // K-slices per item (mq_kernels.hpp schedule). Exact mode keeps the
 // reference's ascending group order per output, so it never splits; token-
-// tiled (prefill) launches are tensor-bound and use one tile per unit. Decode
-// splits sub4 tiles S ways and sub8 tiles 2S ways (equal bytes per unit).
+// tiled (prefill) launches use one tile per unit (and stream-K, below). Decode
+// (best_split, once per layer: it is off the per-call host path) picks the
+// power-of-two split (S4 for sub4 tiles, S8 in {S4, 2 S4} for sub8
+// tiles, whose groups stream twice the bytes) that minimises the busiest CTA's
+// streamed bytes under the persistent grid's round-robin unit assignment, plus
+// a per-unit cost and a reduction cost for split items (cost model in sub4
+// groups; constants measured on the Llama decode shapes).
+void best_split(mq_layer_s* L) {
+    const double kUnitCost = 2.0, kSplitCost = 4.0;
+    const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4;
+    double best = 1e30;
+    for (int S4 = 1; S4 <= 8; S4 *= 2) {
+        for (int S8 = S4; S8 <= 2 * S4; S8 *= 2) {
+            if (S4 > G || S8 > G) continue;
+            const int64_t u8 = T8 * S8, units = u8 + T4 * S4;
+            const int64_t grid = std::min<int64_t>(units, L->num_sms);
+            const double c8 = 2.0 * double(G) / S8 + kUnitCost + (S8 > 1 ? kSplitCost : 0.0);
+            const double c4 = double(G) / S4 + kUnitCost + (S4 > 1 ? kSplitCost : 0.0);
+            double span = 0;
+            for (int64_t b = 0; b < grid; ++b) {  // CTA b runs units b, b + grid, ...
+                const int64_t n = (units - b + grid - 1) / grid;
+                const int64_t n8 = u8 > b ? (u8 - b + grid - 1) / grid : 0;
+                span = std::max(span, double(n8) * c8 + double(n - n8) * c4);
+            }
+            if (span < best - 1e-9) {
+                best = span;
+                L->split4 = S4;
+                L->split8 = S8;
+            }
+        }
+    }
+}
+
 void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
     pl->S4 = pl->S8 = 1;
     if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1 || pl->bn > 32) return;
-    int best = 1;
     if (ksplit >= 2) {
-        best = 1;
+        int best = 1;
         while (best * 2 <= ksplit) best *= 2;  // powers of two
-    } else {
-        // the largest S whose units still fit one round of the persistent grid
-        // (a split reduction on the critical path of a multi-round CTA costs more
-        // than the balance it buys)
-        for (int S = 2; S <= 8; S *= 2) {  // powers of two: the kernel decodes units with shifts
-            if (L->G / S < 2) break;
-            if (2 * S * L->tiles8 + S * L->tiles4 <= L->num_sms) best = S;
-        }
+        pl->S4 = best;
+        pl->S8 = 2 * best;
+        while (pl->S8 > 1 && pl->S8 > L->G) pl->S8 >>= 1;
+        return;
     }
-    pl->S4 = best;
-    // sub8 tiles stream twice the bytes of sub4 tiles: halve them too while
-    // everything still fits one round
-    const bool halve8 = best > 1 || 2 * L->tiles8 + L->tiles4 <= L->num_sms;
-    pl->S8 = halve8 ? 2 * best : 1;
-    while (pl->S8 > 1 && pl->S8 > L->G) pl->S8 >>= 1;
+    pl->S4 = L->split4;  // best_split, computed once per layer
+    pl->S8 = L->split8;
 }
 
 mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
@@ -173,6 +197,11 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn >= 64 && L->G < 256 && items * 256 < (int64_t(1) << 32) &&
         o->schedule != 1 && stream_k_pays(L, pl, o->schedule == 2))
         plan_stream_k(L, pl);
+    static const bool plan_log = std::getenv("MQ_PLAN_LOG") != nullptr;  // development
+    if (plan_log)
+        std::fprintf(stderr, "mq plan: N=%lld K=%lld M=%lld bn=%d tb=%d S4=%d S8=%d units=%d grid=%d sk=%d\n",
+                     (long long)L->N, (long long)L->K, (long long)M, pl->bn, pl->tb, pl->S4, pl->S8, pl->units, pl->grid,
+                     pl->sk ? 1 : 0);
     return MQ_OK;
 }
 
@@ -301,6 +330,7 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     L->n4 = b4 - a4;
     L->tiles8 = (L->n8 + kTileRows - 1) / kTileRows;
     L->tiles4 = (L->n4 + kTileRows - 1) / kTileRows;
+    best_split(L);
     if (o.world > 1) {
         if (mq_status st = mq_shard_plan(d, o.world, &L->shard_cols, nullptr)) {
             delete L;
