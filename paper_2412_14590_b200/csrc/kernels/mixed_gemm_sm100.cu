@@ -201,10 +201,8 @@ __device__ __noinline__ bool sk_piece_done(const GemmParams& p, const Work& wk, 
         for (int j = 0; j < V; ++j)
             __stcg(mine + j * 128, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
         named_bar_sync(2, 128 * NE);
-        if (et == 0) {
-            __threadfence();
+        if (et == 0)  // release: the partial (ordered before by bar.sync) is visible first
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + wk.item), "r"(1u) : "memory");
-        }
         return false;
     }
     // head
@@ -217,8 +215,7 @@ __device__ __noinline__ bool sk_piece_done(const GemmParams& p, const Work& wk, 
         }
         p.cnt[wk.item] = 0u;  // re-arm for the next launch
     }
-    named_bar_sync(2, 128 * NE);
-    __threadfence();
+    named_bar_sync(2, 128 * NE);  // orders the acquire above before every thread's ld.cg below
     const float4* src = part4 + (int64_t(blockIdx.x + 1) * (BN / 4) + c0 / 4) * 128 + r;
     constexpr int VB = V < 8 ? V : 8;  // float4 loads in flight per batch
 #pragma unroll
@@ -797,8 +794,12 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 __stcg(mine + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
             named_bar_sync(2, 128 * NE);
             if (et == 0) {
-                __threadfence();
-                const uint32_t prev = atomicAdd(p.cnt + wk.item, 1u);
+                // release: this CTA's partial (ordered before by bar.sync) is
+                // visible at gpu scope before the count; acquire: the other
+                // slices' partials are visible to the reduction below (ordered
+                // after by bar.sync; ld.cg reads L2) — no full fences
+                uint32_t prev;
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt + wk.item) : "memory");
                 *s_last = prev == uint32_t(wk.S - 1);
                 if (prev == uint32_t(wk.S - 1)) p.cnt[wk.item] = 0u;  // re-arm for the next launch
             }
@@ -806,8 +807,6 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
             const bool last = *s_last != 0;
             named_bar_sync(2, 128 * NE);  // s_last is reused by the next unit
             if (last) {
-                __threadfence();
-                const int col = r < ti.rows ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
                 const float4* base = reinterpret_cast<const float4*>(p.part + int64_t(wk.cta0) * (BN * 128) + r * BN + c0);
                 constexpr int V = BNE / 4;              // float4s per slice
                 constexpr int SB = 32 / BNE;            // slices per batch: every load of a batch in flight
