@@ -286,13 +286,46 @@ def run_ours(args):
         hx = [hx_all]
         hy = [hy_all]
 
+        # per-layer copies on the two copy engines, overlapped with the other
+        # layers' kernels (a pipelined serving step): layer i's forward waits
+        # only for its own input, its output leaves as soon as it is written
+        hxv = list(torch.split(hx_all, nx))
+        hyv = list(torch.split(hy_all, ny))
+        dxf = list(torch.split(dx_all, nx))
+        dyf = list(torch.split(dy_all, ny))
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
         def e2e_step(r):
-            dx_all.copy_(hx_all, non_blocking=True)
+            main = torch.cuda.current_stream(dev)
+            fork = torch.cuda.Event()
+            fork.record(main)
+            s_in.wait_event(fork)
+            s_out.wait_event(fork)
+            ready = []
+            with torch.cuda.stream(s_in):
+                for i in range(len(host)):
+                    dxf[i].copy_(hxv[i], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(s_in)
+                    ready.append(ev)
             for i in range(len(host)):
+                main.wait_event(ready[i])
                 layers[r][i].forward(xv[i], out=yv[i], opts=head["opts"])
-            hy_all.copy_(dy_all, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(main)
+                s_out.wait_event(done)
+                with torch.cuda.stream(s_out):
+                    hyv[i].copy_(dyf[i], non_blocking=True)
+            for st in (s_out, s_in):
+                join = torch.cuda.Event()
+                join.record(st)
+                main.wait_event(join)
 
         efns = graphs_for(e2e_step)
+        t_end = time.time() + 0.3  # pre-ramp clocks, as for the device-resident step
+        while time.time() < t_end:
+            efns[0]()
+            torch.cuda.synchronize()
         ems = timed(efns, args.steps, args.warmup)
         e2e = {"value": head["ops"] / (ems * 1e-3) / 1e12, "unit": "TOPS",
                "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in hx)),
