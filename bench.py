@@ -342,11 +342,39 @@ def run_ours(args):
                 key = f"M{m}" + ("" if ag_name == "group" else "_per_token")
                 t2 = r["ms_k2"] * 1e-3
                 sweep[key] = {"tops": round(r["ops"] / (r["ms"] * 1e-3) / 1e12, 2),
-                              "us_per_layer": round(r["ms"] * 1e3, 2),
-                              "k2_us_per_layer": round(r["ms_k2"] * 1e3, 2),
+                              "us_per_stack": round(r["ms"] * 1e3, 2),
+                              "k2_us_per_stack": round(r["ms_k2"] * 1e3, 2),
                               "k2_hbm_frac": round(r["k2_bytes"] / t2 / 1e9 / hbm_peak, 3),
                               "k2_int8_tc_frac": (round(r["ops"] / t2 / 1e12 / int8_peak, 3) if int8_peak else None)}
                 del r
+
+    # ---- C5 (BASELINE configs[4]): the same stack with the 8-bit fraction swept
+    # 0-20%, at batch 1 and 512 (device-resident, K1 + K2, CUDA graph)
+    c5 = {}
+    if world == 1 and not args.no_sweep:
+        for pct in (0.0, 0.05, 0.20):
+            stack = []
+            for i, (name, N, K) in enumerate(SHAPES_8B):
+                W, _, prom = mq.bench_inputs(1, N, K, pct, 1 + i)
+                stack.append(mq.DeviceLayer(mq.partition_and_quantize(W, prom, name=name), local))
+            for m in (1, 512):
+                xs_p, ys_p, opts_p = make_io(m, GROUP)
+
+                def fwd(r, xs_p=xs_p, ys_p=ys_p, opts_p=opts_p):
+                    for i in range(len(stack)):
+                        stack[i].forward(xs_p[i], out=ys_p[i], opts=opts_p)
+                g = graphs_for(fwd)[0]
+                for _ in range(3):
+                    g()
+                ms_p = timed([g], max(10, args.steps // 4), 3)
+                ops_p = sum(2.0 * m * N * K for (_, N, K, _) in host)
+                c5[f"p{int(round(pct * 100))}_M{m}"] = {"tops": round(ops_p / (ms_p * 1e-3) / 1e12, 2),
+                                                        "us_per_stack": round(ms_p * 1e3, 2)}
+            del stack
+        for m in (1, 512):  # the 10% point is the main sweep's
+            key = f"M{m}"
+            if key in sweep:
+                c5[f"p10_{key}"] = {"tops": sweep[key]["tops"], "us_per_stack": sweep[key]["us_per_stack"]}
 
     # ---- CPU baseline (rank 0, N = 1 only): the reference on the host cores
     cpu = None
@@ -375,6 +403,7 @@ def run_ours(args):
             "int8_peak_tops_measured": round(int8_peak, 1) if int8_peak else None,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps * 2 * len(SHAPES_8B), "clocks": clocks,
             "sweep": sweep,
+            "c5_percent_8bit_sweep": c5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

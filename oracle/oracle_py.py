@@ -335,6 +335,30 @@ class RefLayer:
         self.n8, self.n4 = int(n8[0]), int(n4[0])
         self.group = group
 
+    @classmethod
+    def load_quantized(cls, path: str) -> list:
+        """The reference's load_quantized_model (mixed.cpp:336-370): one layer per linear."""
+        hs = (C.c_void_p * 64)()
+        n = C.c_int(0)
+        dims = np.zeros(128, np.int64)
+        lib = ref()
+        lib.mqref_load_quantized.argtypes = [C.c_char_p, _P, C.c_int, _P, _P]
+        st = lib.mqref_load_quantized(path.encode(), C.cast(hs, _P), 64, C.byref(n), _ptr(dims))
+        if st:
+            raise OracleError(st, lib.mqref_last_error().decode())
+        out = []
+        for i in range(n.value):
+            o = cls.__new__(cls)
+            o.h = C.c_void_p(hs[i])
+            o.N, o.K = int(dims[2 * i]), int(dims[2 * i + 1])
+            n8 = np.zeros(1, np.int64)
+            n4 = np.zeros(1, np.int64)
+            lib.mqref_layer_dims(o.h, _ptr(n8), _ptr(n4))
+            o.n8, o.n4 = int(n8[0]), int(n4[0])
+            o.group = 128
+            out.append(o)
+        return out
+
     def export(self):
         G = (self.K + self.group - 1) // self.group
         map8 = np.zeros(self.n8, np.int32)

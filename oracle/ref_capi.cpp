@@ -9,6 +9,7 @@
 //   quantize_tensor          proj/include/mixquant/quant.hpp:183-243
 //   prepack_weights          proj/src/gemm.cpp:89-108
 //   run_bench                proj/src/gemm.cpp:206-259
+//   save/load_quantized_model proj/src/mixed.cpp:308-370 (quantized.json I/O)
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -156,5 +157,40 @@ int mqref_quantize_tensor(const void* m, int is_double, int64_t rows, int64_t co
 }
 
 float mqref_fast_i2f(int32_t x) { return fast_i2f(x); }
+
+// Writes a "mixquant-quantized-v1" directory with the reference's own writer:
+// the listed layer handles (mqref_layer_create, renamed) as qm.linears.
+int mqref_save_quantized(void* const* layers, const char* const* names, int n_layers, const char* source_model,
+                         double percent, int group, const char* dir) {
+    return guarded([&] {
+        QuantizedModel qm;
+        qm.source_model = source_model;
+        qm.percent = percent;
+        qm.act_scheme = QuantScheme{8, true, group, false};
+        qm.largebit = QuantScheme{8, true, group, false};
+        qm.smallbit = QuantScheme{4, false, group, false};
+        for (int i = 0; i < n_layers; ++i) {
+            MixedLinearLayer l = static_cast<RefLayer*>(layers[i])->layer;
+            l.name = names[i];
+            qm.linears.push_back(std::move(l));
+        }
+        save_quantized_model(qm, dir);
+    });
+}
+
+// The reference's reader: one layer handle per linear (N, K per layer in dims).
+int mqref_load_quantized(const char* dir, void** handles, int max_layers, int* n_layers, int64_t* dims) {
+    return guarded([&] {
+        QuantizedModel qm = load_quantized_model(dir);
+        *n_layers = static_cast<int>(qm.linears.size());
+        for (int i = 0; i < *n_layers && i < max_layers; ++i) {
+            auto* h = new RefLayer;
+            h->layer = std::move(qm.linears[static_cast<size_t>(i)]);
+            dims[2 * i] = h->layer.out_features;
+            dims[2 * i + 1] = h->layer.in_features;
+            handles[i] = h;
+        }
+    });
+}
 
 } // extern "C"

@@ -10,12 +10,15 @@ from .mixquant import (  # noqa: F401
     DataError,
     DeviceLayer,
     MixedLinearLayer,
+    QuantizedModel,
     QuantizedTensor,
     QuantScheme,
     UsageError,
     bench_inputs,
     exec_opts,
     execute_mixed_linear,
+    load_device_layers,
+    load_quantized_model,
     fast_i2f,
     fnv1a_hex,
     pack_nibbles,
@@ -27,6 +30,7 @@ from .mixquant import (  # noqa: F401
     reassemble_output,
     round_scale_f16,
     run_bench,
+    save_quantized_model,
     shard_plan,
     unpack_nibbles,
     validate_mixed_layer,

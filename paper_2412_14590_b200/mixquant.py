@@ -183,6 +183,148 @@ def partition_and_quantize(weight: np.ndarray, promoted, largebit: QuantScheme =
         lib().mq_host_layer_destroy(h)
 
 
+# ------------------------------------------------------- quantized model I/O
+# "mixquant-quantized-v1" directories (mixed.cpp:208-370): quantized.json plus
+# raw little-endian tensors per sub-problem — <layer>.sub{8,4}.codes.bin u8
+# [rows, row_stride], .scales.bin f32 [rows, G], .zero_points.bin u8 [rows, G]
+# (asymmetric only). Empty sub-problems write no files.
+QUANTIZED_FORMAT = "mixquant-quantized-v1"
+
+
+@dataclass
+class QuantizedModel:
+    """QuantizedModel (mixed.hpp:81-88)."""
+    source_model: str = ""
+    percent: float = 0.0
+    act_scheme: QuantScheme = ACT_SCHEME
+    largebit: QuantScheme = LARGEBIT
+    smallbit: QuantScheme = SMALLBIT
+    linears: list = field(default_factory=list)
+
+
+def _scheme_json(s: QuantScheme) -> dict:  # scheme_to_json (mixed.cpp:213-218)
+    return {"bit_width": s.bit_width, "symmetric": bool(s.symmetric), "group_size": s.group_size,
+            "scale_f16_storage": bool(s.scale_f16_storage)}
+
+
+def _scheme_from_json(j) -> QuantScheme:  # scheme_from_json (mixed.cpp:220-228)
+    s = QuantScheme(int(j["bit_width"]), bool(j["symmetric"]), int(j["group_size"]), bool(j["scale_f16_storage"]))
+    if s.bit_width not in (4, 8):  # validate_scheme (quant.cpp:7-16)
+        raise UsageError(f"bit_width must be 4 or 8, got {s.bit_width}")
+    if s.group_size < 1:
+        raise UsageError(f"group_size must be >= 1, got {s.group_size}")
+    return s
+
+
+_DTYPES = {"f64": (np.float64, 8), "f32": (np.float32, 4), "i32": (np.int32, 4), "i8": (np.int8, 1),
+           "u8": (np.uint8, 1)}  # dtype_from_name / dtype_payload_bytes (tensor.cpp:19-39)
+
+
+def save_quantized_model(qm: QuantizedModel, path) -> None:
+    """save_quantized_model (mixed.cpp:308-334) + write_sub (:251-274)."""
+    import json
+    import os
+    os.makedirs(path, exist_ok=True)
+    layers = []
+    for layer in qm.linears:
+        validate_mixed_layer(layer)
+        tensors = {}
+        for tag, sub in (("sub8", layer.sub8), ("sub4", layer.sub4)):
+            if sub.rows == 0:
+                continue
+            prefix = f"{layer.name}.{tag}"
+            roles = [("codes", "u8", np.ascontiguousarray(sub.payload, np.uint8).reshape(sub.rows, -1)),
+                     ("scales", "f32", np.ascontiguousarray(sub.scales, np.float32))]
+            if not sub.scheme.symmetric:
+                roles.append(("zero_points", "u8", np.ascontiguousarray(sub.zero_points, np.uint8)))
+            for role, dt, arr in roles:
+                fname = f"{prefix}.{role}.bin"
+                arr.tofile(os.path.join(path, fname))
+                tensors[f"{prefix}_{role}"] = {"file": fname, "dtype": dt, "shape": [int(d) for d in arr.shape]}
+        layers.append({"name": layer.name, "out_features": int(layer.out_features),
+                       "in_features": int(layer.in_features),
+                       "index_map8": [int(v) for v in layer.index_map8],
+                       "index_map4": [int(v) for v in layer.index_map4], "tensors": tensors})
+    j = {"format": QUANTIZED_FORMAT, "source_model": qm.source_model, "percent": float(qm.percent),
+         "act_scheme": _scheme_json(qm.act_scheme), "largebit": _scheme_json(qm.largebit),
+         "smallbit": _scheme_json(qm.smallbit), "layers": layers}
+    try:
+        with open(os.path.join(path, "quantized.json"), "w") as f:
+            f.write(json.dumps(j, indent=2) + "\n")
+    except OSError as e:
+        raise DataError(f"cannot write quantized manifest in '{path}': {e}") from None
+
+
+def load_quantized_model(path) -> QuantizedModel:
+    """load_quantized_model (mixed.cpp:336-370) + read_sub (:276-306): DataError
+    on a missing or malformed manifest, a tensor whose bytes do not match its
+    declared shape (make_tensor, tensor.cpp:47-61), or a layer that fails
+    validate_mixed_layer."""
+    import json
+    import os
+    manifest = os.path.join(path, "quantized.json")
+    try:
+        with open(manifest) as f:
+            text = f.read()
+    except OSError:
+        raise DataError(f"cannot open '{manifest}'") from None
+    try:
+        j = json.loads(text)
+        qm = QuantizedModel(str(j["source_model"]), float(j["percent"]), _scheme_from_json(j["act_scheme"]),
+                            _scheme_from_json(j["largebit"]), _scheme_from_json(j["smallbit"]))
+
+        def read_tensor(jt, role):
+            ref = jt[role]
+            fname = os.path.join(path, str(ref["file"]))
+            if str(ref["dtype"]) not in _DTYPES:
+                raise DataError(f"unknown dtype '{ref['dtype']}'")
+            dt, width = _DTYPES[str(ref["dtype"])]
+            shape = [int(d) for d in ref["shape"]]
+            if not shape or any(d < 1 for d in shape):
+                raise DataError("tensor dimensions must be >= 1")
+            try:
+                raw = np.fromfile(fname, np.uint8)
+            except OSError:
+                raise DataError(f"cannot open '{fname}'") from None
+            expected = int(np.prod(shape)) * width
+            if raw.size != expected:
+                raise DataError(f"tensor payload is {raw.size} bytes, expected {expected}")
+            return raw.view(dt).reshape(shape)
+
+        def read_sub(jt, prefix, scheme, rows, cols):
+            G = 0 if cols == 0 else (cols + scheme.group_size - 1) // scheme.group_size
+            if rows == 0:
+                stride = cols if scheme.bit_width == 8 else (cols + 1) // 2
+                return QuantizedTensor(scheme, 0, cols, np.zeros((0, stride), np.uint8), np.zeros((0, G), np.float32),
+                                       None if scheme.symmetric else np.zeros((0, G), np.uint8))
+            codes = read_tensor(jt, prefix + "_codes")
+            scales = read_tensor(jt, prefix + "_scales").astype(np.float32, copy=False)
+            zp = None if scheme.symmetric else read_tensor(jt, prefix + "_zero_points").astype(np.uint8, copy=False)
+            return QuantizedTensor(scheme, rows, cols, np.ascontiguousarray(codes.reshape(rows, -1)),
+                                   np.ascontiguousarray(scales), None if zp is None else np.ascontiguousarray(zp))
+
+        for jl in j["layers"]:
+            name = str(jl["name"])
+            N, K = int(jl["out_features"]), int(jl["in_features"])
+            m8 = np.asarray(jl["index_map8"], np.int32)
+            m4 = np.asarray(jl["index_map4"], np.int32)
+            jt = jl["tensors"]
+            layer = MixedLinearLayer(name, N, K, read_sub(jt, name + ".sub8", qm.largebit, m8.size, K),
+                                     read_sub(jt, name + ".sub4", qm.smallbit, m4.size, K), m8, m4)
+            validate_mixed_layer(layer)
+            qm.linears.append(layer)
+        return qm
+    except (DataError, UsageError):
+        raise
+    except (KeyError, TypeError, ValueError, json.JSONDecodeError) as e:
+        raise DataError(f"malformed quantized manifest '{manifest}': {e}") from None
+
+
+def load_device_layers(path, device: int = 0, w8_mode: int = capi.MQ_W8_REFERENCE) -> dict:
+    """quantized.json -> {layer name: DeviceLayer} (each packed once into HBM)."""
+    return {layer.name: DeviceLayer(layer, device, w8_mode=w8_mode) for layer in load_quantized_model(path).linears}
+
+
 def validate_mixed_layer(layer: MixedLinearLayer) -> None:
     check(lib().mq_validate_layer(C.byref(layer.desc())))
 

@@ -237,3 +237,19 @@ def test_cpp_dropin_binary(cuda):
     assert os.path.exists(_build.TEST_BIN), "tests/cpp/_bin/test_dropin not built (run __graft_entry__.build())"
     r = subprocess.run([_build.TEST_BIN, "--gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_quantized_model_device_layers(cuda):
+    """quantized.json written by the reference -> DeviceLayers -> MQ_EXACT forward
+    bit-identical to the oracle on the loaded layers."""
+    import os
+    import torch
+    fx = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "quantized_v1")
+    layers = mq.load_device_layers(fx)
+    assert sorted(layers) == ["blk0.proj", "blk0.pure4"]
+    for name, dl in layers.items():
+        L = dl.layer
+        A = np.random.default_rng(7).standard_normal((9, L.in_features)).astype(np.float32)
+        Y = dl.forward(torch.from_numpy(A).to(cuda), opts=mq.exec_opts(capi.MQ_EXACT, 128)).cpu().numpy()
+        ref, _, _ = O.mixed_linear(_oracle_layer(L), A)
+        assert np.array_equal(Y, ref), name
