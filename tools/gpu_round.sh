@@ -11,6 +11,7 @@ if [ "$2" != "skip-tests" ]; then
 fi
 timeout 300 python tools/quick_time.py > gpurun_out/quick_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/quick_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/bench_$TAG.log
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ref_$TAG.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-sweep --no-cpu > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:mixed_gemm -s 3 -c 2 \
