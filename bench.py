@@ -396,7 +396,7 @@ def run_ours(args):
                        "l2": "2 device replicas of the stack (~256 MB) alternate between steps (> 126 MB L2)",
                        "cuda_graph": world == 1},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                         "frac": round(achieved / hbm_peak, 4), "traffic": k2_traffic(M),
                          "kernel": f"mixed_gemm_tc_kernel ({len(SHAPES_8B)} launches/step; bytes and time summed)",
                          "peak_kind": peak_kind,
                          "k2_bytes_per_step": int(head["k2_bytes"]), "k2_ms_per_step": round(head["ms_k2"], 5)},
@@ -473,6 +473,20 @@ def run_reference(args):
     if budget_steps != args.steps:
         line["note"] = f"steps capped at {budget_steps} (each step is the whole CPU stack)"
     print(json.dumps(line), flush=True)
+
+
+def k2_traffic(m):
+    """DRAM bytes (read + write) per step of the K2 launches from the committed ncu
+    launch list of this workload (profiles/r1/k2_traffic.json, written by
+    tools/launch_summary.py from `ncu --metrics dram__bytes_*`); None when absent
+    or for another batch."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "k2_traffic.json")
+    if m != 16 or not os.path.exists(path):
+        return None
+    try:
+        return int(json.load(open(path))["k2_dram_bytes_per_step"])
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def main():

@@ -12,7 +12,7 @@ fi
 timeout 300 python tools/quick_time.py > gpurun_out/quick_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/quick_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/bench_$TAG.log
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ref_$TAG.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-sweep --no-cpu > gpurun_out/ncu_launch_$TAG.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:mixed_gemm -s 3 -c 2 \
    -o gpurun_out/prof_k2_$TAG -f python tools/ncu_target.py 14336 4096 16 > gpurun_out/ncu_full_$TAG.log 2>&1
