@@ -34,7 +34,8 @@ struct mq_layer_s {
     int64_t shard_cols = 0;
     int w8_mode = MQ_W8_REFERENCE;
     int64_t tiles8 = 0, tiles4 = 0;
-    int split4 = 1, split8 = 1;         // decode K-split chosen once at create (choose_split)
+    int split4[3] = {1, 1, 1};          // K-split chosen once at create (choose_split) for token
+    int split8[3] = {1, 1, 1};          // tiles <= 32 (decode), 64 and 128 (one token block)
     uint8_t* d_wq = nullptr;
     int32_t* d_colmap = nullptr;
     int64_t bytes_wq = 0, stream_bytes = 0;
@@ -75,16 +76,19 @@ struct Plan {
 // Stream-K plan (mq_kernels.hpp): equal cost per CTA over the item sequence,
 // boundaries rounded down to the tile's chunk size. Used by FAST token-tiled
 // launches when the unit schedule's last round would leave CTAs idle for
-// longer than a cut item costs; every CTA gets >= 2 items of work, so an item
-// is cut at most once (head + tail, sk_piece_done).
+// longer than a cut item costs; every CTA range covers at least one item's
+// length, so an item is cut at most once (head + tail, sk_piece_done).
 bool stream_k_pays(const mq_layer_s* L, const Plan* pl, bool force) {
     const int64_t G = L->G, items = int64_t(pl->tb) * (L->tiles8 + L->tiles4);
     const int grid = std::min<int>(L->num_sms, kSkMax);
     const double per_cta = double(items * G) / grid;  // groups (prefill: a sub8 group costs as a sub4 one)
-    if (per_cta < 2.0 * G) return false;
+    // every CTA range (less the chunk rounding of its ends) must cover a whole
+    // item's length, so no item is cut twice (head + tail, sk_piece_done)
+    if (per_cta < double(G + 2 * gemm_gps(pl->bn) + 1)) return false;
     if (force) return true;
     const int64_t rounds = (items + grid - 1) / grid;
-    const double cut_cost = 16.0;  // measured: publish + join + tail of a cut item ~ 16 groups
+    // measured (BN = 64 and 128): publish + join + tail of a cut item ~ 16 groups
+    const double cut_cost = 16.0;
     return per_cta + cut_cost < double(rounds * G);
 }
 
@@ -126,8 +130,11 @@ void plan_stream_k(const mq_layer_s* L, Plan* pl) {
 // streamed bytes under the persistent grid's round-robin unit assignment, plus
 // a per-unit cost and a reduction cost for split items (cost model in sub4
 // groups; constants measured on the Llama decode shapes).
-void best_split(mq_layer_s* L) {
-    const double kUnitCost = 2.0, kSplitCost = 4.0;
+// kind 0: decode token tiles, where a sub8 group streams twice a sub4 group's
+// bytes; kind 1 / 2: 64 / 128-token tiles, where every group costs the same
+// rescale work and a split join moves a 32 / 64 KB partial
+void best_split(mq_layer_s* L, int kind) {
+    const double kUnitCost = 2.0, kSplitCost = kind == 0 ? 4.0 : kind == 1 ? 8.0 : 16.0, k8 = kind == 0 ? 2.0 : 1.0;
     const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4;
     double best = 1e30;
     for (int S4 = 1; S4 <= 8; S4 *= 2) {
@@ -135,7 +142,7 @@ void best_split(mq_layer_s* L) {
             if (S4 > G || S8 > G) continue;
             const int64_t u8 = T8 * S8, units = u8 + T4 * S4;
             const int64_t grid = std::min<int64_t>(units, L->num_sms);
-            const double c8 = 2.0 * double(G) / S8 + kUnitCost + (S8 > 1 ? kSplitCost : 0.0);
+            const double c8 = k8 * double(G) / S8 + kUnitCost + (S8 > 1 ? kSplitCost : 0.0);
             const double c4 = double(G) / S4 + kUnitCost + (S4 > 1 ? kSplitCost : 0.0);
             double span = 0;
             for (int64_t b = 0; b < grid; ++b) {  // CTA b runs units b, b + grid, ...
@@ -145,8 +152,8 @@ void best_split(mq_layer_s* L) {
             }
             if (span < best - 1e-9) {
                 best = span;
-                L->split4 = S4;
-                L->split8 = S8;
+                L->split4[kind] = S4;
+                L->split8[kind] = S8;
             }
         }
     }
@@ -154,7 +161,7 @@ void best_split(mq_layer_s* L) {
 
 void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
     pl->S4 = pl->S8 = 1;
-    if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1 || pl->bn > 32) return;
+    if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1) return;
     if (ksplit >= 2) {
         int best = 1;
         while (best * 2 <= ksplit) best *= 2;  // powers of two
@@ -163,8 +170,9 @@ void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
         while (pl->S8 > 1 && pl->S8 > L->G) pl->S8 >>= 1;
         return;
     }
-    pl->S4 = L->split4;  // best_split, computed once per layer
-    pl->S8 = L->split8;
+    const int kind = pl->bn <= 32 ? 0 : pl->bn == 64 ? 1 : 2;  // best_split, computed once per layer
+    pl->S4 = L->split4[kind];
+    pl->S8 = L->split8[kind];
 }
 
 mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
@@ -194,7 +202,8 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     // stream-K when the unit schedule's last round would leave CTAs idle
     if (o->schedule < 0 || o->schedule > 2) return fail(MQ_USAGE, "schedule must be 0 (auto), 1 (units) or 2 (stream-K)");
     const int64_t items = int64_t(pl->tb) * (L->tiles8 + L->tiles4);
-    if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn >= 64 && L->G < 256 && items * 256 < (int64_t(1) << 32) &&
+    if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn >= 64 && pl->S4 == 1 && pl->S8 == 1 && L->G < 256 &&
+        items * 256 < (int64_t(1) << 32) &&
         o->schedule != 1 && stream_k_pays(L, pl, o->schedule == 2))
         plan_stream_k(L, pl);
     static const bool plan_log = std::getenv("MQ_PLAN_LOG") != nullptr;  // development
@@ -215,7 +224,7 @@ EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
     EalWs w;
     const size_t items = size_t(pl.tb) * size_t(L->tiles8 + L->tiles4);
-    w.off_part = al(items * 4);
+    w.off_part = 2 * al(items * 4);  // counters | generations
     const bool split = pl.S4 > 1 || pl.S8 > 1;
     const size_t slots = pl.sk ? size_t(pl.grid) + 1 : split ? size_t(pl.units) : 0;
     w.off_acts = w.off_part + al(slots * 128 * size_t(pl.bn) * 4);
@@ -330,7 +339,7 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     L->n4 = b4 - a4;
     L->tiles8 = (L->n8 + kTileRows - 1) / kTileRows;
     L->tiles4 = (L->n4 + kTileRows - 1) / kTileRows;
-    best_split(L);
+    for (int kind = 0; kind < 3; ++kind) best_split(L, kind);
     if (o.world > 1) {
         if (mq_status st = mq_shard_plan(d, o.world, &L->shard_cols, nullptr)) {
             delete L;
@@ -477,6 +486,7 @@ mq_status launch_k2(mq_layer_s* L, const Plan& pl, const void* ws, int64_t M, vo
     gemm_params(L, pl, M, Y, out_dtype, &p);
     p.cnt = reinterpret_cast<uint32_t*>(base);
     p.part = reinterpret_cast<float*>(base + w.off_part);
+    p.gen = reinterpret_cast<uint32_t*>(base + w.off_part / 2);
     p.acts = base + w.off_acts;
     p.sa = reinterpret_cast<const float*>(base + w.off_sa);
     p.asum = reinterpret_cast<const int32_t*>(base + w.off_asum);

@@ -182,8 +182,8 @@ __device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& l
     hi = (((w >> 4) & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
 }
 
-// Stream-K split piece epilogue. The plan gives every CTA at least two items
-// of work, so an item is cut at most once: its HEAD (groups [0, g)) is the last
+// Stream-K split piece epilogue. Every CTA's range covers at least one item's
+// length (host plan), so an item is cut at most once: its HEAD (groups [0, g)) is the last
 // piece of CTA b and its TAIL (groups [g, G)) the first piece of CTA b + 1,
 // which finishes it long before CTA b reaches the head. The tail publishes its
 // partial tile to slot b + 1 ([slot][BN/4][128] float4: a warp's stores are 512
@@ -232,6 +232,84 @@ __device__ __noinline__ bool sk_piece_done(const GemmParams& p, const Work& wk, 
         }
     }
     return true;
+}
+
+// K-split join for wide token tiles (BN >= 64, one token block, MQ_FAST): the
+// S slices of an item publish their partial tiles to slot = unit
+// ([slot][BN/4][128] float4, coalesced). When every unit runs in one round of
+// the persistent grid (all slices co-resident) the slices meet at a per-item
+// barrier (arrival counter + generation, sense reversing) and each one sums and
+// scatters only ITS BN/S tokens — the scattered stores drain at ~25 cycles per
+// warp instruction, so one CTA storing the whole tile would be the launch's
+// tail. Otherwise the last arrival sums and scatters the whole tile. Sums run
+// in slice order (deterministic). Out of line: its registers would push the
+// 64-accumulator epilogue loop into spills.
+template <int BN, int BNE, int NE, int MODE>
+__device__ __noinline__ void split_join_wide(const GemmParams& p, const Work& wk, int slot, float* acc, int r,
+                                             int c0, int et, volatile int* s_last, int col, int64_t m0) {
+    constexpr int V = BNE / 4;
+    float4* part4 = reinterpret_cast<float4*>(p.part);
+    float4* mine = part4 + (int64_t(slot) * (BN / 4) + c0 / 4) * 128 + r;
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+        __stcg(mine + j * 128, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
+    named_bar_sync(2, 128 * NE);
+    const bool together = p.units <= int(gridDim.x);
+    if (et == 0) {
+        if (together) {
+            volatile uint32_t* gen = p.gen + wk.item;
+            const uint32_t g0 = *gen;  // read before arriving: the barrier cannot pass without us
+            uint32_t prev;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt + wk.item) : "memory");
+            if (prev == uint32_t(wk.S - 1)) {
+                p.cnt[wk.item] = 0u;  // re-arm, then release the others
+                __threadfence();
+                atomicAdd(p.gen + wk.item, 1u);
+            } else {
+                while (*gen == g0) __nanosleep(20);
+                __threadfence();
+            }
+        } else {  // release our partial / acquire the others' (see the decode join)
+            uint32_t prev;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt + wk.item) : "memory");
+            *s_last = prev == uint32_t(wk.S - 1);
+            if (prev == uint32_t(wk.S - 1)) p.cnt[wk.item] = 0u;  // re-arm for the next launch
+        }
+    }
+    named_bar_sync(2, 128 * NE);
+    // token range this CTA sums and scatters: its slice's share, or the whole tile
+    int j0 = 0, j1 = BNE;
+    if (together) {
+        const int t0 = wk.sl * (BN / wk.S), t1 = t0 + BN / wk.S;
+        j0 = (t0 > c0 ? t0 : c0) - c0;
+        j1 = (t1 < c0 + BNE ? t1 : c0 + BNE) - c0;
+        if (j1 <= j0) return;
+    } else {
+        const bool last = *s_last != 0;
+        named_bar_sync(2, 128 * NE);  // s_last is reused by the next unit
+        if (!last) return;
+    }
+    for (int j = j0; j < j1; j += 4) {  // float4 of tokens j..j+3 (BN/S is a multiple of 4)
+        float4 sum = __ldcg(part4 + (int64_t(wk.cta0) * (BN / 4) + (c0 + j) / 4) * 128 + r);
+        for (int sl = 1; sl < wk.S; ++sl) {
+            const float4 t = __ldcg(part4 + (int64_t(wk.cta0 + sl) * (BN / 4) + (c0 + j) / 4) * 128 + r);
+            sum.x = __fadd_rn(sum.x, t.x);
+            sum.y = __fadd_rn(sum.y, t.y);
+            sum.z = __fadd_rn(sum.z, t.z);
+            sum.w = __fadd_rn(sum.w, t.w);
+        }
+        if (col < 0) continue;
+        const float v4[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+        for (int e4 = 0; e4 < 4; ++e4) {
+            const int64_t m = m0 + j + e4;
+            if (m < p.M) {
+                float v = v4[e4];
+                if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
+                store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
+            }
+        }
+    }
 }
 
 template <int BN, int MODE>
@@ -787,6 +865,13 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
             // [128][BN] (slot = unit; a thread's tokens are contiguous -> float4),
             // count arrivals; the last slice sums all S partials in slice order
             // (deterministic) and scatters them
+            if constexpr (BN >= 64 && (MODE == kFastGroup || MODE == kFastToken)) {
+                float tmp[BNE];
+#pragma unroll
+                for (int j = 0; j < BNE; ++j) tmp[j] = acc[j];
+                split_join_wide<BN, BNE, NE, MODE>(p, wk, U.key, tmp, r, c0, et, s_last, col, m0);
+                continue;
+            }
             if constexpr (BN <= 32) {
             float4* mine = reinterpret_cast<float4*>(p.part + int64_t(U.key) * (BN * 128) + r * BN + c0);
 #pragma unroll

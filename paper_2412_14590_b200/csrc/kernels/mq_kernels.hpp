@@ -75,6 +75,7 @@ struct GemmParams {
     int32_t grid;           // persistent CTAs (<= SMs): CTA b runs units b, b + grid, ...
     float* part;            // split-K partial tiles [units][BN][128] (slot = unit index)
     uint32_t* cnt;          // arrival counters [TB * (T8 + T4)], zero between launches
+    uint32_t* gen;          // per-item barrier generations [TB * (T8 + T4)] (any value)
     int32_t rotate;         // 1: each CTA starts its K loop at a CTA-dependent chunk (FAST modes)
     uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int32_t* partials;      // dump mode

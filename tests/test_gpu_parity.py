@@ -137,6 +137,25 @@ def test_fast_mode_within_tolerance(cuda, m):
     assert _rel(Y, ref) <= TOL
 
 
+@pytest.mark.parametrize("m,n,k", [(64, 512, 2048), (96, 640, 2048), (128, 1024, 1536)])
+def test_fast_mode_wide_tile_k_split(cuda, m, n, k):
+    """One wide token tile (BN 64/128) on a narrow layer: the K-split join of
+    the 64/128-token partials (split_join_wide), within tolerance and
+    bit-reproducible run to run."""
+    import torch
+    L, A = _layer(m, n, k, 0.1, seed=31)
+    dl = mq.DeviceLayer(L)
+    o = mq.exec_opts(capi.MQ_FAST, 128)
+    dA = torch.from_numpy(A).to(cuda)
+    Y = dl.forward(dA, opts=o).cpu().numpy()
+    ref, _, _ = O.mixed_linear(_oracle_layer(L), A)
+    assert _rel(Y, ref) <= TOL
+    for ks in (2, 4):  # explicit splits through the same join
+        assert _rel(dl.forward(dA, opts=mq.exec_opts(capi.MQ_FAST, 128, ksplit=ks)).cpu().numpy(), ref) <= TOL
+    for _ in range(2):
+        assert np.array_equal(dl.forward(dA, opts=o).cpu().numpy(), Y)
+
+
 @pytest.mark.parametrize("m,tt,sched", [(576, 64, 2), (1100, 128, 2), (1100, 128, 1), (1100, 128, 0)])
 def test_fast_mode_stream_k(cuda, m, tt, sched):
     """Stream-K schedule (cut items summed head + tail) vs unit rounds: both

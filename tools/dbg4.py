@@ -27,6 +27,8 @@ for i, nm in enumerate(names):
     col = a[:, i]
     print(f"{nm:16s} min {np.nanmin(col):7.2f} med {np.nanmedian(col):7.2f} max {np.nanmax(col):7.2f} us")
 
+order = np.argsort(-np.nan_to_num(a[:, 5], nan=-1))[:6]
+print("slowest CTAs (epi_exit):", [(int(i), round(float(a[i, 5]), 2), round(float(a[i, 4]), 2)) for i in order])
 ch = raw[148*8:].reshape(16, 64)
 b = min(v for v in ch[:8].reshape(-1) if v > 0)
 print("CTA chunk timeline (kcycles): issue / mma_start / mma_commit / conv_done / epi_done / conv_full / conv_waits / mma_wfull / mma_wx / mma_wa / xprod_issue / store_begin / store_end / epi_start")

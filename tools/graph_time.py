@@ -14,7 +14,7 @@ for (N, K) in SH:
     L = mq.partition_and_quantize(W, prom)
     reps = [mq.DeviceLayer(L) for _ in range(2)]
     dA = torch.from_numpy(A).cuda()
-    opts = mq.exec_opts(capi.MQ_FAST, 128)
+    opts = mq.exec_opts(capi.MQ_FAST, 128, ksplit=int(os.environ.get("KSPLIT", "0")), schedule=int(os.environ.get("SCHED", "0")))
     wss = [r.quantize_ws(dA, opts) for r in reps]
     Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
     for i in range(4):
@@ -35,4 +35,4 @@ for (N, K) in SH:
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / 200
     wb = reps[0].info.weight_stream_bytes
-    print(f"dbg={os.environ.get('MQ_DBG', '0'):>3s} N={N} K={K} M={M}: {us:6.2f} us/launch  {wb / us / 1e3:6.0f} GB/s", flush=True)
+    print(f"sched={os.environ.get('SCHED', '0')} ks={os.environ.get('KSPLIT', '0')} dbg={os.environ.get('MQ_DBG', '0'):>3s} N={N} K={K} M={M}: {us:6.2f} us/launch  {wb / us / 1e3:6.0f} GB/s", flush=True)
