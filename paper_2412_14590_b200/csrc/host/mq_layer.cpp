@@ -159,9 +159,38 @@ void best_split(mq_layer_s* L, int kind) {
     }
 }
 
+// The same model for tb > 1 token blocks of wide tiles when there are fewer
+// items than SMs (prefill on a narrow layer): explicit round-robin over the
+// tb x (sub8 slices, sub4 slices) unit sequence (<= 8 x #SM units).
+void best_split_blocks(const mq_layer_s* L, int kind, int tb, int* S4o, int* S8o) {
+    const double kUnitCost = 2.0, kSplitCost = kind == 1 ? 8.0 : 16.0;
+    const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4;
+    double best = 1e30;
+    std::vector<double> cta(size_t(L->num_sms));
+    for (int S = 1; S <= 8; S *= 2) {
+        if (S > G) break;
+        const int64_t per_tb = (T8 + T4) * S, units = per_tb * tb;
+        const int64_t grid = std::min<int64_t>(units, L->num_sms);
+        std::fill(cta.begin(), cta.end(), 0.0);
+        const double c = double(G) / S + kUnitCost + (S > 1 ? kSplitCost : 0.0);
+        for (int64_t u = 0; u < units; ++u) cta[size_t(u % grid)] += c;
+        const double span = *std::max_element(cta.begin(), cta.begin() + grid);
+        if (span < best - 1e-9) {
+            best = span;
+            *S4o = *S8o = S;
+        }
+    }
+}
+
 void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
     pl->S4 = pl->S8 = 1;
-    if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1 || pl->tb > 1) return;
+    if (pl->mode == kExactGroup || pl->mode == kExactToken || ksplit == 1) return;
+    if (pl->tb > 1) {
+        const int64_t items = int64_t(pl->tb) * (L->tiles8 + L->tiles4);
+        if (pl->bn > 32 && ksplit == 0 && items < L->num_sms)
+            best_split_blocks(L, pl->bn == 64 ? 1 : 2, pl->tb, &pl->S4, &pl->S8);
+        return;
+    }
     if (ksplit >= 2) {
         int best = 1;
         while (best * 2 <= ksplit) best *= 2;  // powers of two
