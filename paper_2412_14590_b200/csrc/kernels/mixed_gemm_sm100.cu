@@ -312,7 +312,10 @@ __device__ __noinline__ void split_join_wide(const GemmParams& p, const Work& wk
     }
 }
 
-template <int BN, int MODE>
+// SPL = 1: the wide-tile K-split join is compiled in (launched only for split
+// unit schedules of 64/128-token tiles; its out-of-line call costs the other
+// wide launches ~4% in the accumulation loop's register allocation)
+template <int BN, int MODE, int SPL>
 __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(const __grid_constant__ GemmParams p) {
     using C = TcCfg<BN>;
     constexpr int NS = C::NS, NE = C::NE, BNE = C::BNE, GPS = C::GPS, NA = C::NA, NT = C::NT, NC = C::NC;
@@ -847,31 +850,28 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 if (et == 0) trace_chunk(p, 12, n);
                 continue;
             }
-            if constexpr (MODE == kFastGroup || MODE == kFastToken) {
-            if (p.sk) {
-                // stream-K split piece (out of line: its registers would push
-                // the accumulation loop into spills)
+            if constexpr (BN >= 64 && (MODE == kFastGroup || MODE == kFastToken)) {
+                // a split piece of a wide tile, out of line (its registers would
+                // push the 64-accumulator loop into spills): stream-K head / tail
+                // (the head scatters the joined tile from registers here), or a
+                // K-slice of the unit schedule
                 float tmp[BNE];
 #pragma unroll
                 for (int j = 0; j < BNE; ++j) tmp[j] = acc[j];
-                if (!sk_piece_done<BN, BNE, NE>(p, wk, tmp, r, c0, et)) continue;
+                if constexpr (SPL) {
+                    split_join_wide<BN, BNE, NE, MODE>(p, wk, U.key, tmp, r, c0, et, s_last, col, m0);
+                } else {
+                    if (!sk_piece_done<BN, BNE, NE>(p, wk, tmp, r, c0, et)) continue;
 #pragma unroll
-                for (int j = 0; j < BNE; ++j) acc[j] = tmp[j];
-                store_acc();
+                    for (int j = 0; j < BNE; ++j) acc[j] = tmp[j];
+                    store_acc();
+                }
                 continue;
-            }
             }
             // split-K (decode token tiles only): publish this slice's partial tile
             // [128][BN] (slot = unit; a thread's tokens are contiguous -> float4),
             // count arrivals; the last slice sums all S partials in slice order
             // (deterministic) and scatters them
-            if constexpr (BN >= 64 && (MODE == kFastGroup || MODE == kFastToken)) {
-                float tmp[BNE];
-#pragma unroll
-                for (int j = 0; j < BNE; ++j) tmp[j] = acc[j];
-                split_join_wide<BN, BNE, NE, MODE>(p, wk, U.key, tmp, r, c0, et, s_last, col, m0);
-                continue;
-            }
             if constexpr (BN <= 32) {
             float4* mine = reinterpret_cast<float4*>(p.part + int64_t(U.key) * (BN * 128) + r * BN + c0);
 #pragma unroll
@@ -941,15 +941,14 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     }
 }
 
-template <int BN, int MODE>
-cudaError_t launch_bn_mode(const GemmParams& p, bool pdl, cudaStream_t stream) {
+template <int BN, void (*KERN)(GemmParams)>
+cudaError_t launch_kernel(const GemmParams& p, bool pdl, cudaStream_t stream) {
     using C = TcCfg<BN>;
-    auto kern = mixed_gemm_tc_kernel<BN, MODE>;
-    static thread_local uint64_t configured = 0;  // per device ordinal bitmask
+    static thread_local uint64_t configured = 0;  // per kernel: device ordinal bitmask
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured >> dev & 1)) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
         configured |= uint64_t(1) << dev;
     }
@@ -964,7 +963,15 @@ cudaError_t launch_bn_mode(const GemmParams& p, bool pdl, cudaStream_t stream) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, p);
+    return cudaLaunchKernelEx(&cfg, KERN, p);
+}
+
+template <int BN, int MODE>
+cudaError_t launch_bn_mode(const GemmParams& p, bool pdl, cudaStream_t stream) {
+    if constexpr (BN >= 64 && (MODE == kFastGroup || MODE == kFastToken)) {
+        if (!p.sk && (p.S4 > 1 || p.S8 > 1)) return launch_kernel<BN, mixed_gemm_tc_kernel<BN, MODE, 1>>(p, pdl, stream);
+    }
+    return launch_kernel<BN, mixed_gemm_tc_kernel<BN, MODE, 0>>(p, pdl, stream);
 }
 
 template <int BN>
