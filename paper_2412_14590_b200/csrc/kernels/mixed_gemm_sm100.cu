@@ -91,10 +91,14 @@ struct TcCfg {
 #define MQ_NS_MAX 8
 #endif
     static constexpr int NS = NS0 > MQ_NS_MAX ? MQ_NS_MAX : NS0;
-    // epilogue warpgroups: two at decode too — one warp per SMSP would leave the
-    // TMEM-load / rescale chain latency-bound
-    static constexpr int NE = (BN == 16 || BN >= 128) ? 2 : 1;
-    static constexpr int NC = BN <= 32 ? 2 : 1;  // converter warpgroups (decode is conversion-bound)
+    // epilogue warpgroups: two (one at BN = 64, where a second measured ~2%
+    // slower) — one warp per SMSP leaves the TMEM-load / rescale chain
+    // latency-bound (A/B at 32-token tiles: 6-18% faster with two)
+    static constexpr int NE = BN == 64 ? 1 : 2;
+    // converter warpgroups: two at 16-token tiles (conversion-bound); from 32
+    // tokens the rescale dominates and one warpgroup converts fast enough
+    // (A/B: 32-token launches 6-23% faster with one)
+    static constexpr int NC = BN == 16 ? 2 : 1;
     static constexpr int BNE = BN / NE;          // tokens per epilogue warpgroup
     static constexpr int kEpiThread0 = 128 * (1 + NC);
     static constexpr int kThreads = 128 * (1 + NC + NE);
