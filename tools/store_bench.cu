@@ -7,7 +7,17 @@
 #include <random>
 #include <cuda_fp16.h>
 
-template <int MODE>
+template <int OP>
+__device__ __forceinline__ void st16(__half* p, __half v) {
+    const unsigned short b = __half_as_ushort(v);
+    if (OP == 0) *p = v;
+    else if (OP == 1) asm volatile("st.global.cg.u16 [%0], %1;" ::"l"(p), "h"(b) : "memory");
+    else if (OP == 2) asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(b) : "memory");
+    else if (OP == 3) asm volatile("st.global.wt.u16 [%0], %1;" ::"l"(p), "h"(b) : "memory");
+    else asm volatile("st.global.L1::no_allocate.u16 [%0], %1;" ::"l"(p), "h"(b) : "memory");
+}
+
+template <int MODE, int OP = 0>
 __global__ void __launch_bounds__(256) scatter(__half* Y, const int* colmap, int N, int M, int tiles, int units) {
     const int r = threadIdx.x & 127, e = threadIdx.x >> 7;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -21,7 +31,7 @@ __global__ void __launch_bounds__(256) scatter(__half* Y, const int* colmap, int
 #pragma unroll
             for (int j = 0; j < 64; ++j) {
                 const long m = long(tb) * 128 + e * 64 + j;
-                if (m < M) Y[m * N + col] = __float2half_rn(acc[j]);
+                if (m < M) st16<OP>(Y + m * N + col, __float2half_rn(acc[j]));
             }
         }
     }
@@ -59,6 +69,25 @@ int main() {
                             mode == 0 ? "scatter, back-to-back" : mode == 1 ? "contiguous" : mode == 2 ? "scatter, Y cold" : "scatter, Y warm",
                             ms * 1e3, M * double(N) * 2 / ms / 1e6);
         }
+    }
+    const char* names[5] = {"default", "st.cg", "st.cs", "st.wt", "L1::no_allocate"};
+    for (int op = 0; op < 5; ++op) {
+        float best = 1e9;
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(a);
+            switch (op) {
+                case 0: scatter<0, 0><<<148, 256>>>(Y, dcm, N, M, tiles, units); break;
+                case 1: scatter<0, 1><<<148, 256>>>(Y, dcm, N, M, tiles, units); break;
+                case 2: scatter<0, 2><<<148, 256>>>(Y, dcm, N, M, tiles, units); break;
+                case 3: scatter<0, 3><<<148, 256>>>(Y, dcm, N, M, tiles, units); break;
+                default: scatter<0, 4><<<148, 256>>>(Y, dcm, N, M, tiles, units); break;
+            }
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            best = ms < best ? ms : best;
+        }
+        printf("scatter %-16s: %.2f us\n", names[op], best * 1e3);
     }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
