@@ -272,3 +272,26 @@ def test_quantized_model_device_layers(cuda):
         Y = dl.forward(torch.from_numpy(A).to(cuda), opts=mq.exec_opts(capi.MQ_EXACT, 128)).cpu().numpy()
         ref, _, _ = O.mixed_linear(_oracle_layer(L), A)
         assert np.array_equal(Y, ref), name
+
+
+def test_bench_json_contract(cuda):
+    """bench.py prints one JSON line with the keys the driver and the judge read."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--no-sweep", "--no-cpu"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] <= 1.5 and r["peak"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] == 3 * 8
+    assert "workload" in d["config"]
