@@ -295,3 +295,29 @@ def test_bench_json_contract(cuda):
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 3 * 8
     assert "workload" in d["config"]
+
+
+@pytest.mark.parametrize("m,n,k,tt,sched,ag", [(1100, 4096, 1024, 128, 2, 1024), (96, 640, 2048, 0, 0, 2048),
+                                               (300, 1024, 1000, 128, 2, 128)])
+def test_fast_mode_split_paths_per_token_and_ragged(cuda, m, n, k, tt, sched, ag):
+    """Per-token activations (s_a applied after the K join) through stream-K and
+    the wide-tile K-split, and a ragged last K-group through stream-K."""
+    import torch
+    L, A = _layer(m, n, k, 0.1, seed=41)
+    dl = mq.DeviceLayer(L)
+    o = mq.exec_opts(capi.MQ_FAST, ag, token_tile=tt, schedule=sched)
+    Y = dl.forward(torch.from_numpy(A).to(cuda), opts=o).cpu().numpy()
+    ref, _, _ = O.mixed_linear(_oracle_layer(L), A, act_group=None if ag == 128 else ag)
+    assert _rel(Y, ref) <= TOL
+
+
+def test_bf16_output_wide_split(cuda):
+    """bf16 output through the wide-tile K-split join equals the f32 result rounded once."""
+    import torch
+    L, A = _layer(96, 640, 2048, 0.1, seed=43)
+    dl = mq.DeviceLayer(L)
+    dA = torch.from_numpy(A).to(cuda)
+    o = mq.exec_opts(capi.MQ_FAST, 128)
+    y32 = dl.forward(dA, opts=o).cpu()
+    y16 = dl.forward(dA, opts=o, out_dtype=torch.bfloat16).cpu()
+    assert torch.equal(y16.float(), y32.to(torch.bfloat16).float())
