@@ -188,6 +188,13 @@ mq_status mq_layer_shard_colmap(mq_layer_t layer, int32_t* out);
 mq_status mq_quantize_act(const void* A, mq_dtype a_dtype, int64_t M, int64_t K, int64_t lda,
                           int32_t group_size, int8_t* codes, int64_t ldc, float* scales,
                           int64_t lds, int32_t* err, void* stream);
+/* The same with the reference's full activation scheme (quantize_tensor<float>
+ * with a QuantScheme, quant.hpp:183-185): scheme must be {8, symmetric,
+ * group_size, scale_f16_storage}; scale_f16_storage rounds each scale to the
+ * binary16 grid (round_scale_f16, quant.cpp:81-86). */
+mq_status mq_quantize_act_scheme(const void* A, mq_dtype a_dtype, int64_t M, int64_t K, int64_t lda,
+                                 const mq_scheme* scheme, int8_t* codes, int64_t ldc, float* scales,
+                                 int64_t lds, int32_t* err, void* stream);
 
 /* Forward modes.
  * MQ_EXACT: per output element the K-groups run in ascending order with an f32
@@ -207,6 +214,17 @@ typedef struct {
     int32_t no_pdl;      /* 1 = plain launches (default: programmatic dependent launch) */
     int32_t schedule;    /* MQ_FAST token-tiled launches: 0 = auto, 1 = unit rounds, 2 = stream-K
                             (equal work per SM; each cut item summed head + tail) where it applies */
+    int32_t concurrent;  /* 1 = other kernels may hold SMs during this launch (multi-stream use,
+                            overlapped collectives): never use a schedule whose CTAs wait on each
+                            other (the one-round wide-tile barrier join); 0 = the launch owns the
+                            device while it runs (default, fastest) */
+    int32_t act_scale_f16; /* the activation scheme's scale_f16_storage (quant.hpp:70-76,
+                              quant.cpp:81-86): round activation scales to binary16 */
+    const struct mq_layer_s* prefetch_next; /* optional: the layer the caller runs NEXT on this
+                            stream; once this launch has issued its own weight reads, its CTAs
+                            prefetch the head of that layer's packed weights into L2 (weights
+                            are immutable, so this is safe under any data dependency) */
+    int64_t prefetch_bytes; /* bytes of prefetch_next to prefetch (0 = auto) */
 } mq_exec_opts;
 
 /* Bytes of scratch a forward needs: split-K arrival counters + partial tiles
@@ -223,8 +241,10 @@ size_t mq_forward_workspace_bytes(mq_layer_t layer, int64_t M, const mq_exec_opt
  * Y: device [M, out_features] row-major in out_dtype (sharded layers: the
  * rank's [M, shard_cols] block in gather order).
  * workspace: device, >= mq_forward_workspace_bytes, zero-initialised once
- * before first use (the engine leaves it zeroed). NULL uses the layer's own
- * (then calls on one layer must be stream-serialised). */
+ * before first use. Its first 64 KiB are split-K arrival counters that every
+ * launch leaves at zero, so one workspace can serve any M, any layer and any
+ * options, as long as launches that share it are stream-ordered. NULL uses the
+ * layer's own (then calls on one layer must be stream-serialised). */
 mq_status mq_mixed_linear_codes(mq_layer_t layer, const int8_t* codes, int64_t ldc,
                                 const float* scales, int64_t lds, int64_t M, void* Y,
                                 mq_dtype out_dtype, const mq_exec_opts* opts, void* workspace,
@@ -241,8 +261,11 @@ size_t mq_mixed_linear_workspace_bytes(mq_layer_t layer, int64_t M, const mq_exe
 /* Split form of mq_mixed_linear for callers that feed ONE quantized activation
  * to several layers with the same K, M and options (e.g. separate q/k/v or
  * gate/up layers): mq_quantize_act_ws runs K1 into the engine activation layout
- * (EAL) inside `workspace` (>= mq_mixed_linear_workspace_bytes); then any number
- * of mq_mixed_linear_ws calls run K2 on it. Same results as mq_mixed_linear. */
+ * (EAL) inside `workspace`; then any number of mq_mixed_linear_ws calls, on
+ * any of those layers, run K2 on it. The EAL sits at an offset that depends
+ * only on (K, M, options); each layer's split-K partials follow it, so the
+ * workspace must be >= the MAXIMUM of mq_mixed_linear_workspace_bytes over the
+ * layers that share it. Same results as mq_mixed_linear. */
 mq_status mq_quantize_act_ws(mq_layer_t layer, const void* A, mq_dtype a_dtype, int64_t M,
                              const mq_exec_opts* opts, void* workspace, int32_t* err, void* stream);
 mq_status mq_mixed_linear_ws(mq_layer_t layer, int64_t M, const void* workspace, void* Y,

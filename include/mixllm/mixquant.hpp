@@ -364,7 +364,8 @@ class DeviceLayer {
 // Host f32 A -> host f32 Y through the device (synchronous): the common body
 // of the value-returning drop-ins. group_size = the activation group (the
 // weight group, or K for the per-token extension).
-inline MatrixRMf forward_host(DeviceLayer& dl, const MatrixRMf& A, int act_group, mq_mode mode = MQ_EXACT) {
+inline MatrixRMf forward_host(DeviceLayer& dl, const MatrixRMf& A, int act_group, mq_mode mode = MQ_EXACT,
+                              bool act_scale_f16 = false) {
     const Index M = A.rows(), K = A.cols(), N = dl.info().out_features;
     MatrixRMf Y(M, N);
     if (M == 0) return Y;
@@ -375,6 +376,7 @@ inline MatrixRMf forward_host(DeviceLayer& dl, const MatrixRMf& A, int act_group
     mq_exec_opts o{};
     o.mode = mode;
     o.act_group = act_group;
+    o.act_scale_f16 = act_scale_f16 ? 1 : 0;
     dl.forward(dA.get(), MQ_F32, M, dY.get(), MQ_F32, o, static_cast<int32_t*>(dErr.get()), nullptr);
     int32_t err = 0;
     MQ_CUDA_CHECK(cudaMemcpy(&err, dErr.get(), 4, cudaMemcpyDeviceToHost));  // synchronises the default stream
@@ -399,7 +401,7 @@ inline MatrixRMf execute_mixed_linear(const MatrixRMf& activations, const MixedL
         throw UsageError("execute_mixed_linear: activations must use an 8-bit symmetric scheme");
     if (activations.cols() != layer.in_features) throw UsageError("activation columns != in_features");
     b200::DeviceLayer dl(layer);
-    return b200::forward_host(dl, activations, act_scheme.group_size);
+    return b200::forward_host(dl, activations, act_scheme.group_size, MQ_EXACT, act_scheme.scale_f16_storage);
 }
 
 // execute_mixed_on_codes (gemm.cpp:140-181): already-quantized activations

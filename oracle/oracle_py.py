@@ -97,6 +97,7 @@ def ref():
         lib.mqref_layer_export.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P]
         lib.mqref_layer_prepack.argtypes = [_P, C.c_int, _P]
         lib.mqref_layer_forward.argtypes = [_P, _P, _I64, C.c_int, C.c_int, _P, _P]
+        lib.mqref_layer_forward_f16.argtypes = [_P, _P, _I64, C.c_int, C.c_int, C.c_int, _P, _P]
         lib.mqref_quantize_tensor.argtypes = [_P, C.c_int, _I64, _I64, C.c_int, C.c_int, C.c_int,
                                               C.c_int, _P, _P, _P]
         lib.mqref_fast_i2f.restype = C.c_float
@@ -262,9 +263,9 @@ def prepack(q: QTensor) -> np.ndarray:
     return out
 
 
-def quantize_acts(A: np.ndarray, group: int):
-    """Activation quantization {8, sym, group} (gemm.cpp:190); group=K is per-token."""
-    q = quantize_tensor(np.ascontiguousarray(A, np.float32), 8, True, group)
+def quantize_acts(A: np.ndarray, group: int, f16: bool = False):
+    """Activation quantization {8, sym, group, f16} (gemm.cpp:190); group=K is per-token."""
+    q = quantize_tensor(np.ascontiguousarray(A, np.float32), 8, True, group, f16)
     return q.payload.view(np.int8).copy(), q.scales
 
 
@@ -305,11 +306,12 @@ def reassemble(y8, y4, map8, map4, N: int) -> np.ndarray:
 
 
 def mixed_linear(layer: Layer, A: np.ndarray, act_group: int | None = None, fast: bool = True,
-                 w8_unsigned: bool = True):
+                 w8_unsigned: bool = True, act_f16: bool = False):
     """execute_mixed_linear (gemm.cpp:183-192). act_group = K selects the
-    per-token extension (s_a broadcast across groups). Returns (Y, codes, scales)."""
+    per-token extension (s_a broadcast across groups); act_f16 the activation
+    scheme's scale_f16_storage. Returns (Y, codes, scales)."""
     act_group = layer.group if act_group is None else act_group
-    codes, scales = quantize_acts(A, act_group)
+    codes, scales = quantize_acts(A, act_group, act_f16)
     y8 = gemm_sub(codes, scales, layer.sub8, fast, w8_unsigned) if layer.sub8.rows else np.zeros((A.shape[0], 0), np.float32)
     y4 = gemm_sub(codes, scales, layer.sub4, fast) if layer.sub4.rows else np.zeros((A.shape[0], 0), np.float32)
     return reassemble(y8, y4, layer.map8, layer.map4, layer.N), codes, scales
@@ -380,12 +382,12 @@ class RefLayer:
             raise OracleError(st, ref().mqref_last_error().decode())
         return out
 
-    def forward(self, A: np.ndarray, fast: bool = True, workers: int = 1):
+    def forward(self, A: np.ndarray, fast: bool = True, workers: int = 1, act_f16: bool = False):
         A = np.ascontiguousarray(A, np.float32)
         out = np.zeros((A.shape[0], self.N), np.float32)
         ms = np.zeros(1, np.float64)
-        st = ref().mqref_layer_forward(self.h, _ptr(A), A.shape[0], int(fast), workers,
-                                       _ptr(out), _ptr(ms))
+        st = ref().mqref_layer_forward_f16(self.h, _ptr(A), A.shape[0], int(act_f16), int(fast), workers,
+                                           _ptr(out), _ptr(ms))
         if st:
             raise OracleError(st, ref().mqref_last_error().decode())
         return out, float(ms[0])

@@ -116,15 +116,16 @@ int mqref_layer_prepack(void* hv, int which, uint8_t* out) {
 
 // The reference forward. Times exactly the execute_mixed_linear call
 // (activation quantization + per-call prepack + GEMM + scatter).
-int mqref_layer_forward(void* hv, const float* A, int64_t m, int fast, int workers, float* out,
-                        double* ms) {
+// execute_mixed_linear with the activation scheme {8, sym, layer group, act_f16}.
+int mqref_layer_forward_f16(void* hv, const float* A, int64_t m, int act_f16, int fast, int workers, float* out,
+                            double* ms) {
     auto* h = static_cast<RefLayer*>(hv);
     return guarded([&] {
         MatrixRMf a(m, h->layer.in_features);
         std::memcpy(a.data(), A, sizeof(float) * static_cast<size_t>(a.size()));
         QuantScheme act{8, true, h->layer.sub4.rows > 0 ? h->layer.sub4.scheme.group_size
                                                           : h->layer.sub8.scheme.group_size,
-                        false};
+                        act_f16 != 0};
         const auto t0 = std::chrono::steady_clock::now();
         MatrixRMf y = execute_mixed_linear(a, h->layer, act, TileConfig{},
                                            fast ? I2FMode::Fast : I2FMode::Native, workers);
@@ -132,6 +133,10 @@ int mqref_layer_forward(void* hv, const float* A, int64_t m, int fast, int worke
         if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         std::memcpy(out, y.data(), sizeof(float) * static_cast<size_t>(y.size()));
     });
+}
+
+int mqref_layer_forward(void* hv, const float* A, int64_t m, int fast, int workers, float* out, double* ms) {
+    return mqref_layer_forward_f16(hv, A, m, 0, fast, workers, out, ms);
 }
 
 // quantize_tensor on a float (activation) or double (weight) matrix.

@@ -51,7 +51,8 @@ class mq_layer_info(C.Structure):
 
 class mq_exec_opts(C.Structure):
     _fields_ = [("mode", I32), ("act_group", I32), ("ksplit", I32), ("token_tile", I32), ("gemm_impl", I32),
-                ("no_pdl", I32), ("schedule", I32)]
+                ("no_pdl", I32), ("schedule", I32), ("concurrent", I32), ("act_scale_f16", I32),
+                ("prefetch_next", P), ("prefetch_bytes", I64)]
 
 
 # name -> (restype, argtypes); mirrors capi.h one to one.
@@ -78,6 +79,7 @@ PROTOTYPES = {
     "mq_layer_get_info": (C.c_int, [P, C.POINTER(mq_layer_info)]),
     "mq_layer_shard_colmap": (C.c_int, [P, P]),
     "mq_quantize_act": (C.c_int, [P, C.c_int, I64, I64, I64, I32, P, I64, P, I64, P, P]),
+    "mq_quantize_act_scheme": (C.c_int, [P, C.c_int, I64, I64, I64, C.POINTER(mq_scheme), P, I64, P, I64, P, P]),
     "mq_forward_workspace_bytes": (C.c_size_t, [P, I64, C.POINTER(mq_exec_opts)]),
     "mq_mixed_linear_codes": (C.c_int, [P, P, I64, P, I64, I64, P, C.c_int, C.POINTER(mq_exec_opts), P, P]),
     "mq_mixed_linear": (C.c_int, [P, P, C.c_int, I64, P, C.c_int, C.POINTER(mq_exec_opts), P, P, P]),

@@ -44,6 +44,8 @@ struct mq_layer_s {
     std::mutex mu;                      // guards the internal workspace
     void* d_ws = nullptr;               // internal scratch (workspace = NULL)
     size_t ws_bytes = 0;
+    std::vector<void*> retired;         // outgrown internal workspaces: freed at destroy, never
+                                        // while a launch queued by another caller may use them
 };
 
 namespace {
@@ -69,7 +71,9 @@ int auto_token_tile(int64_t M) {
 struct Plan {
     int bn, tb, mode, per_token, S4, S8, units, grid;
     int64_t Mpad;
-    bool pdl, rotate, sk;
+    bool pdl, rotate, sk, no_spin, f16;
+    const mq_layer_s* pf_layer;
+    int64_t pf_bytes;
     std::vector<uint32_t> skb;  // stream-K boundaries [grid + 1]
 };
 
@@ -210,11 +214,21 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     const int act_group = o->act_group ? o->act_group : L->group;
     if (act_group == L->group && act_group < L->K) pl->per_token = 0;
     else if (act_group >= L->K) pl->per_token = 1;
+    else if (act_group < 1)
+        return fail(MQ_USAGE, "act_group must be >= 1");
     else
         return fail(MQ_USAGE, "activations and weights must share group boundaries (act group " +
                                   std::to_string(act_group) + ", weight group " + std::to_string(L->group) +
                                   "); per-token activations use act_group = K");
     if (o->mode != MQ_EXACT && o->mode != MQ_FAST) return fail(MQ_USAGE, "unknown mode");
+    if (pl->per_token && L->K > kPerTokenKMax)
+        return fail(MQ_USAGE, "per-token activations support K <= " + std::to_string(kPerTokenKMax) + " (K = " +
+                                  std::to_string(L->K) + "); use group-wise activations (act_group = group size)");
+    pl->no_spin = o->concurrent != 0;
+    pl->f16 = o->act_scale_f16 != 0;
+    pl->pf_layer = o->prefetch_next;
+    pl->pf_bytes = o->prefetch_bytes;
+    if (pl->pf_bytes < 0) return fail(MQ_USAGE, "prefetch_bytes must be >= 0");
     if (o->ksplit < 0 || o->ksplit > 8) return fail(MQ_USAGE, "ksplit must be 0 (auto), 1 (none) or a split <= 8");
     pl->bn = o->token_tile ? o->token_tile : auto_token_tile(M);
     if (pl->bn != 16 && pl->bn != 32 && pl->bn != 64 && pl->bn != 128)
@@ -243,24 +257,29 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     return MQ_OK;
 }
 
-// Forward workspace: split-K arrival counters (zero between launches; the
-// kernel re-arms them) | split-K partial tiles | EAL codes [G][Mpad][128] |
-// EAL scales [Ga][Mpad] | EAL code sums [G][Mpad] int32.
+// Forward workspace. [0, 32 KiB): arrival counters (kCntWords; every launch
+// leaves them zero) | EAL codes [G][Mpad][128] | EAL scales [Ga][Mpad] | EAL
+// code sums [G][Mpad] int32 | split-K / stream-K partial tiles. The counter
+// region is the same for every layer and M, and the EAL offsets depend only on
+// (K, Mpad, per_token): one workspace serves any sequence of launches (any M)
+// and one quantized activation feeds several layers (mq_quantize_act_ws).
 struct EalWs {
-    size_t off_part, off_acts, off_sa, off_asum, total;
+    size_t off_acts, off_sa, off_asum, off_part, off_part2, total;
 };
 EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
     EalWs w;
-    const size_t items = size_t(pl.tb) * size_t(L->tiles8 + L->tiles4);
-    w.off_part = 2 * al(items * 4);  // counters | generations
-    const bool split = pl.S4 > 1 || pl.S8 > 1;
-    const size_t slots = pl.sk ? size_t(pl.grid) + 1 : split ? size_t(pl.units) : 0;
-    w.off_acts = w.off_part + al(slots * 128 * size_t(pl.bn) * 4);
+    w.off_acts = size_t(kCntWords) * 4;
     w.off_sa = w.off_acts + al(size_t(L->G) * size_t(pl.Mpad) * 128);
     const int64_t Ga = pl.per_token ? 1 : L->G;
     w.off_asum = w.off_sa + al(size_t(Ga) * size_t(pl.Mpad) * 4);
-    w.total = w.off_asum + al(size_t(L->G) * size_t(pl.Mpad) * 4);
+    w.off_part = w.off_asum + al(size_t(L->G) * size_t(pl.Mpad) * 4);
+    const bool split = pl.S4 > 1 || pl.S8 > 1;
+    const size_t tile = 128 * size_t(pl.bn) * 4;
+    // stream-K: tail partials [grid + 1] then head partials [grid + 1]
+    const size_t slots = pl.sk ? size_t(pl.grid) + 1 : split ? size_t(pl.units) : 0;
+    w.off_part2 = w.off_part + al(slots * tile);
+    w.total = w.off_part2 + (pl.sk ? al(slots * tile) : 0);
     return w;
 }
 
@@ -292,6 +311,13 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dty
     p->sk = pl.sk ? 1 : 0;
     if (pl.sk) std::copy(pl.skb.begin(), pl.skb.end(), p->skb);
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
+    if (pl.pf_layer && pl.pf_layer != L && pl.pf_layer->device == L->device) {
+        // auto: the whole next layer, up to a third of L2 (the weight stream of
+        // this launch is read evict-first, so prefetched lines survive it)
+        const int64_t cap = pl.pf_bytes ? pl.pf_bytes : int64_t(40) << 20;
+        p->pf = pl.pf_layer->d_wq;
+        p->pf_bytes = std::min<int64_t>(cap, pl.pf_layer->bytes_wq) / 256 * 256;
+    }
     static const int dbg = [] {
         const char* e = std::getenv("MQ_DBG");
         return e ? std::atoi(e) : 0;
@@ -315,11 +341,15 @@ mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, cudaStream_t stream, v
         cudaStreamCaptureStatus cs;
         if (stream && cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
             return fail(MQ_USAGE, "internal workspace cannot grow during graph capture; pass a workspace");
-        if (L->d_ws) cudaFree(L->d_ws);
+        // the outgrown buffer may still be referenced by launches queued on other
+        // streams: keep it until the layer is destroyed
+        if (L->d_ws) L->retired.push_back(L->d_ws);
         L->d_ws = nullptr;
         L->ws_bytes = 0;
-        CU_TRY(cudaMalloc(&L->d_ws, bytes));
-        CU_TRY(cudaMemset(L->d_ws, 0, bytes));
+        void* buf = nullptr;
+        CU_TRY(cudaMalloc(&buf, bytes));
+        CU_TRY(cudaMemset(buf, 0, bytes));
+        L->d_ws = buf;
         L->ws_bytes = bytes;
     }
     *ws = L->d_ws;
@@ -368,6 +398,12 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     L->n4 = b4 - a4;
     L->tiles8 = (L->n8 + kTileRows - 1) / kTileRows;
     L->tiles4 = (L->n4 + kTileRows - 1) / kTileRows;
+    if (L->tiles8 + L->tiles4 > kCntWords) {
+        const int64_t T = L->tiles8 + L->tiles4;
+        delete L;
+        return fail(MQ_USAGE, "layer has " + std::to_string(T) + " 128-row tiles per rank; the engine supports " +
+                                  std::to_string(kCntWords) + " (shard it over more ranks)");
+    }
     for (int kind = 0; kind < 3; ++kind) best_split(L, kind);
     if (o.world > 1) {
         if (mq_status st = mq_shard_plan(d, o.world, &L->shard_cols, nullptr)) {
@@ -460,6 +496,7 @@ void mq_layer_destroy(mq_layer_t L) {
     cudaFree(L->d_wq);
     cudaFree(L->d_colmap);
     if (L->d_ws) cudaFree(L->d_ws);
+    for (void* b : L->retired) cudaFree(b);
     delete L;
 }
 
@@ -500,6 +537,23 @@ mq_status mq_quantize_act(const void* A, mq_dtype dt, int64_t M, int64_t K, int6
     return MQ_OK;
 }
 
+mq_status mq_quantize_act_scheme(const void* A, mq_dtype dt, int64_t M, int64_t K, int64_t lda, const mq_scheme* sc,
+                                 int8_t* codes, int64_t ldc, float* scales, int64_t lds, int32_t* err, void* stream) {
+    if (!sc) return fail(MQ_USAGE, "scheme is null");
+    // check_engine_inputs (gemm.cpp:43-45): activations must be 8-bit symmetric
+    if (sc->bit_width != 8 || !sc->symmetric) return fail(MQ_USAGE, "activation scheme must be 8-bit symmetric");
+    if (M < 0 || K < 1) return fail(MQ_USAGE, "bad activation shape");
+    if (sc->group_size < 1) return fail(MQ_USAGE, "group_size must be >= 1");
+    if (lda < K || ldc < K) return fail(MQ_USAGE, "leading dimension smaller than K");
+    if (sc->group_size < K && lds < M) return fail(MQ_USAGE, "scales leading dimension smaller than M");
+    if (dt != MQ_F32 && dt != MQ_F16 && dt != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
+    const int group = sc->group_size >= K ? int(K) : sc->group_size;
+    cudaError_t e = launch_act_quant(A, dt, M, K, lda, group, sc->scale_f16_storage ? 1 : 0, codes, ldc, scales, lds,
+                                     err, true, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
+    return MQ_OK;
+}
+
 size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
     Plan pl;
     if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK) return 0;
@@ -515,7 +569,8 @@ mq_status launch_k2(mq_layer_s* L, const Plan& pl, const void* ws, int64_t M, vo
     gemm_params(L, pl, M, Y, out_dtype, &p);
     p.cnt = reinterpret_cast<uint32_t*>(base);
     p.part = reinterpret_cast<float*>(base + w.off_part);
-    p.gen = reinterpret_cast<uint32_t*>(base + w.off_part / 2);
+    p.part2 = reinterpret_cast<float*>(base + w.off_part2);
+    p.no_spin = pl.no_spin ? 1 : 0;
     p.acts = base + w.off_acts;
     p.sa = reinterpret_cast<const float*>(base + w.off_sa);
     p.asum = reinterpret_cast<const int32_t*>(base + w.off_asum);
@@ -582,7 +637,7 @@ mq_status mq_mixed_linear(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t
     if (o && o->gemm_impl == 1) return fail(MQ_USAGE, "the SIMT debug kernel takes quantized codes (mq_mixed_linear_codes)");
     int32_t* asum = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(ws) + w.off_asum);
     cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad, acts,
-                                         sa, asum, err, pl.pdl, s);
+                                         sa, asum, err, pl.f16 ? 1 : 0, pl.pdl, s);
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
     return launch_k2(L, pl, ws, M, Y, out_dtype, s);
 }
@@ -599,7 +654,7 @@ mq_status mq_quantize_act_ws(mq_layer_t L, const void* A, mq_dtype a_dtype, int6
     uint8_t* base = static_cast<uint8_t*>(ws);
     cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad,
                                          base + w.off_acts, reinterpret_cast<float*>(base + w.off_sa),
-                                         reinterpret_cast<int32_t*>(base + w.off_asum), err, pl.pdl,
+                                         reinterpret_cast<int32_t*>(base + w.off_asum), err, pl.f16 ? 1 : 0, pl.pdl,
                                          static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
     return MQ_OK;

@@ -111,13 +111,13 @@ __global__ void __launch_bounds__(256) act_quant_row_kernel(
 template <int DT>
 __global__ void act_quant_eal_group_kernel(const void* __restrict__ A, int64_t M, int64_t K, int64_t lda, int G,
                                            int64_t Mpad, uint8_t* __restrict__ acts, float* __restrict__ sa,
-                                           int32_t* __restrict__ asum, int32_t* err) {
+                                           int32_t* __restrict__ asum, int32_t* err, int f16) {
     griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
     griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (wid >= Mpad * G) return;
     const int g = static_cast<int>(wid / Mpad);
-    quant_pair_eal<DT>(A, M, K, lda, G, Mpad, acts, sa, asum, err, wid - int64_t(g) * Mpad, g, threadIdx.x & 31);
+    quant_pair_eal<DT>(A, M, K, lda, G, Mpad, acts, sa, asum, err, wid - int64_t(g) * Mpad, g, threadIdx.x & 31, f16);
 }
 
 // per-token (group == K): one CTA per token row m < Mpad
@@ -129,7 +129,7 @@ template <int DT, int RV>
 __global__ void __launch_bounds__(1024) act_quant_eal_row_kernel(const void* __restrict__ A, int64_t M, int64_t K,
                                                                  int64_t lda, int G, int64_t Mpad,
                                                                  uint8_t* __restrict__ acts, float* __restrict__ sa,
-                                                                 int32_t* __restrict__ asum, int32_t* err) {
+                                                                 int32_t* __restrict__ asum, int32_t* err, int f16) {
     griddep_launch();  // the dependent GEMM may start its prologue + weight prefetch now
     griddep_wait();    // the previous kernel's outputs (our inputs) are complete
     __shared__ float red[32];
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(1024) act_quant_eal_row_kernel(const void* __r
         anybad |= bad[i];
     }
     if (live && anybad && threadIdx.x == 0 && err) atomicMin(err, static_cast<int32_t>(m));
-    const float s = live ? act_scale(amax, 0) : 0.0f;
+    const float s = live ? act_scale(amax, f16) : 0.0f;
     // a warp's 32 x 4 codes of step v are exactly one 128-wide group
 #pragma unroll
     for (int v = 0; v < RV; ++v) {
@@ -246,15 +246,15 @@ cudaError_t launch_ex(K kern, dim3 grid, dim3 block, bool pdl, cudaStream_t stre
 }  // namespace
 
 cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda, int group,
-                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum, int32_t* err, bool pdl,
-                                 cudaStream_t stream) {
+                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum, int32_t* err, int f16,
+                                 bool pdl, cudaStream_t stream) {
     if (Mpad == 0) return cudaSuccess;
     const int G = static_cast<int>((K + 127) / 128);
     if (group >= K) {
         const dim3 grid(static_cast<unsigned>(Mpad));
         const int64_t steps = (K + 4095) / 4096;  // 1024 threads x 4 values per step
         if (steps > 8) return cudaErrorInvalidValue;  // K > 32768: not a Llama shape
-#define MQ_ROW(DT, RV) launch_ex(act_quant_eal_row_kernel<DT, RV>, grid, dim3(1024), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err)
+#define MQ_ROW(DT, RV) launch_ex(act_quant_eal_row_kernel<DT, RV>, grid, dim3(1024), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16)
 #define MQ_ROWS(DT) (steps <= 1 ? MQ_ROW(DT, 1) : steps <= 2 ? MQ_ROW(DT, 2) : steps <= 4 ? MQ_ROW(DT, 4) : MQ_ROW(DT, 8))
         switch (a_dtype) {
             case 0: return MQ_ROWS(0);
@@ -267,9 +267,9 @@ cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t 
     const int64_t warps = Mpad * G;
     const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));
     switch (a_dtype) {
-        case 0: return launch_ex(act_quant_eal_group_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
-        case 1: return launch_ex(act_quant_eal_group_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
-        default: return launch_ex(act_quant_eal_group_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err);
+        case 0: return launch_ex(act_quant_eal_group_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
+        case 1: return launch_ex(act_quant_eal_group_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
+        default: return launch_ex(act_quant_eal_group_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
     }
 }
 

@@ -188,45 +188,59 @@ __device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& l
 
 // Stream-K split piece epilogue. Every CTA's range covers at least one item's
 // length (host plan), so an item is cut at most once: its HEAD (groups [0, g)) is the last
-// piece of CTA b and its TAIL (groups [g, G)) the first piece of CTA b + 1,
-// which finishes it long before CTA b reaches the head. The tail publishes its
-// partial tile to slot b + 1 ([slot][BN/4][128] float4: a warp's stores are 512
-// contiguous bytes) and raises the item's flag; the head waits for the flag
-// (co-resident persistent grid: no deadlock), adds the tail's partial to its
-// own (head + tail: one rounding, order-independent, deterministic) and
-// returns true so the caller scatters the sum. Returns false for a tail.
+// piece of CTA b and its TAIL (groups [g, G)) the first piece of CTA b + 1.
+// The two meet without any spin-wait (no co-residency assumption): boundary
+// s = b + 1 owns flag cnt[s] and two partial slots ([slot][BN/4][128] float4,
+// a warp's stores are 512 contiguous bytes), tails in p.part, heads in
+// p.part2. The tail publishes its partial and arrives; the head (which almost
+// always runs later) first checks the flag: if the tail is done it adds the
+// tail's partial without publishing its own; otherwise it publishes and
+// arrives. Whoever arrives second sums head + tail (one f32 add: commutative,
+// so the result is the same bit pattern either way) and returns true so the
+// caller scatters; it also re-arms the flag for the next launch.
 template <int BN, int BNE, int NE>
-__device__ __noinline__ bool sk_piece_done(const GemmParams& p, const Work& wk, float* acc, int r, int c0, int et) {
+__device__ __noinline__ bool sk_piece_done(const GemmParams& p, const Work& wk, float* acc, int r, int c0, int et,
+                                           volatile int* s_last) {
     constexpr int V = BNE / 4;
-    float4* part4 = reinterpret_cast<float4*>(p.part);
-    if (wk.g0 > 0) {  // tail
-        float4* mine = part4 + (int64_t(blockIdx.x) * (BN / 4) + c0 / 4) * 128 + r;
+    const bool tail = wk.g0 > 0;
+    const int s = int(blockIdx.x) + (tail ? 0 : 1);
+    float4* mine = reinterpret_cast<float4*>(tail ? p.part : p.part2) + (int64_t(s) * (BN / 4) + c0 / 4) * 128 + r;
+    const float4* other = reinterpret_cast<const float4*>(tail ? p.part2 : p.part) + (int64_t(s) * (BN / 4) + c0 / 4) * 128 + r;
+    int mode = 0;  // 0: publish and arrive, 2: head that found the tail done
+    if (!tail) {
+        if (et == 0) {
+            uint32_t f;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(p.cnt + s) : "memory");
+            if (f) p.cnt[s] = 0u;  // both pieces are here: re-arm
+            *s_last = f ? 2 : 0;
+        }
+        named_bar_sync(2, 128 * NE);  // orders the acquire before every thread's ld.cg below
+        mode = *s_last;
+        named_bar_sync(2, 128 * NE);  // s_last is rewritten below
+    }
+    bool last = mode == 2;
+    if (!last) {
 #pragma unroll
         for (int j = 0; j < V; ++j)
             __stcg(mine + j * 128, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
         named_bar_sync(2, 128 * NE);
-        if (et == 0)  // release: the partial (ordered before by bar.sync) is visible first
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.cnt + wk.item), "r"(1u) : "memory");
-        return false;
-    }
-    // head
-    if (et == 0) {
-        uint32_t f = 0;
-        for (;;) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(p.cnt + wk.item) : "memory");
-            if (f) break;
-            __nanosleep(64);
+        if (et == 0) {  // release our partial (ordered before by bar.sync) / acquire the other's
+            uint32_t prev;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt + s) : "memory");
+            if (prev == 1u) p.cnt[s] = 0u;  // second arrival: re-arm
+            *s_last = prev == 1u;
         }
-        p.cnt[wk.item] = 0u;  // re-arm for the next launch
+        named_bar_sync(2, 128 * NE);
+        last = *s_last != 0;
+        named_bar_sync(2, 128 * NE);  // s_last is reused by the next unit
+        if (!last) return false;
     }
-    named_bar_sync(2, 128 * NE);  // orders the acquire above before every thread's ld.cg below
-    const float4* src = part4 + (int64_t(blockIdx.x + 1) * (BN / 4) + c0 / 4) * 128 + r;
     constexpr int VB = V < 8 ? V : 8;  // float4 loads in flight per batch
 #pragma unroll
     for (int j0 = 0; j0 < V; j0 += VB) {
         float4 t[VB];
 #pragma unroll
-        for (int q = 0; q < VB; ++q) t[q] = __ldcg(src + (j0 + q) * 128);
+        for (int q = 0; q < VB; ++q) t[q] = __ldcg(other + (j0 + q) * 128);
 #pragma unroll
         for (int q = 0; q < VB; ++q) {
             acc[4 * (j0 + q) + 0] = __fadd_rn(acc[4 * (j0 + q) + 0], t[q].x);
@@ -242,7 +256,7 @@ __device__ __noinline__ bool sk_piece_done(const GemmParams& p, const Work& wk, 
 // S slices of an item publish their partial tiles to slot = unit
 // ([slot][BN/4][128] float4, coalesced). When every unit runs in one round of
 // the persistent grid (all slices co-resident) the slices meet at a per-item
-// barrier (arrival counter + generation, sense reversing) and each one sums and
+// barrier (arrivals then departures on one counter) and each one sums and
 // scatters only ITS BN/S tokens — the scattered stores drain at ~25 cycles per
 // warp instruction, so one CTA storing the whole tile would be the launch's
 // tail. Otherwise the last arrival sums and scatters the whole tile. Sums run
@@ -258,21 +272,23 @@ __device__ __noinline__ void split_join_wide(const GemmParams& p, const Work& wk
     for (int j = 0; j < V; ++j)
         __stcg(mine + j * 128, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
     named_bar_sync(2, 128 * NE);
-    const bool together = p.units <= int(gridDim.x);
+    // the per-item barrier assumes every slice is resident: only when all units
+    // run in one round and the caller did not declare concurrent launches
+    const bool together = p.units <= int(gridDim.x) && !p.no_spin;
     if (et == 0) {
         if (together) {
-            volatile uint32_t* gen = p.gen + wk.item;
-            const uint32_t g0 = *gen;  // read before arriving: the barrier cannot pass without us
-            uint32_t prev;
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt + wk.item) : "memory");
-            if (prev == uint32_t(wk.S - 1)) {
-                p.cnt[wk.item] = 0u;  // re-arm, then release the others
-                __threadfence();
-                atomicAdd(p.gen + wk.item, 1u);
-            } else {
-                while (*gen == g0) __nanosleep(20);
-                __threadfence();
+            // arrivals count to S, departures to 2S; the last departure re-arms
+            // the counter (every slice has seen >= S by then), so it is zero
+            // again at launch end and no generation word is needed
+            uint32_t* c = p.cnt + wk.item;
+            uint32_t prev, v;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(c) : "memory");
+            for (v = prev + 1; v < uint32_t(wk.S);) {
+                __nanosleep(20);
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
             }
+            asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(c) : "memory");
+            if (prev == uint32_t(2 * wk.S - 1)) *c = 0u;
         } else {  // release our partial / acquire the others' (see the decode join)
             uint32_t prev;
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt + wk.item) : "memory");
@@ -463,6 +479,15 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 rr.next<NS>();
             }
         }
+        // every weight read of this launch is issued: warm L2 with the next
+        // layer's weights (its first-byte latency and this launch's tail overlap)
+        if (p.pf_bytes > 0 && elect_one()) {
+            const int64_t per = ((p.pf_bytes + gridDim.x - 1) / gridDim.x + 255) / 256 * 256;
+            int64_t a = int64_t(blockIdx.x) * per;
+            const int64_t e = a + per < p.pf_bytes ? a + per : p.pf_bytes;
+            for (; a < e; a += 32768) ptx::bulk_prefetch_l2(p.pf + a, uint32_t(e - a < 32768 ? e - a : 32768));
+        }
+        __syncwarp();
         if (lane == 0) trace(p, 1);
     } else if (warp == 2) {
         // ===================== activation producer (EAL tiles) =====================
@@ -865,7 +890,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 if constexpr (SPL) {
                     split_join_wide<BN, BNE, NE, MODE>(p, wk, U.key, tmp, r, c0, et, s_last, col, m0);
                 } else {
-                    if (!sk_piece_done<BN, BNE, NE>(p, wk, tmp, r, c0, et)) continue;
+                    if (!sk_piece_done<BN, BNE, NE>(p, wk, tmp, r, c0, et, s_last)) continue;
 #pragma unroll
                     for (int j = 0; j < BNE; ++j) acc[j] = tmp[j];
                     store_acc();

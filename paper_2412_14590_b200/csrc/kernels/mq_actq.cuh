@@ -1,6 +1,5 @@
-// mq_actq.cuh — the K1 per-(token, group) arithmetic shared by the standalone
-// activation-quantization kernels (act_quant.cu) and the decode GEMM's fused
-// prologue (mixed_gemm_sm100.cu). Restates quantize_group_sym<float>
+// mq_actq.cuh — the K1 per-(token, group) arithmetic of the activation-
+// quantization kernels (act_quant.cu). Restates quantize_group_sym<float>
 // (proj/include/mixquant/quant.hpp:117-140) bit for bit: see act_quant.cu.
 #pragma once
 #include <cuda_bf16.h>
@@ -65,7 +64,8 @@ __device__ __forceinline__ void load4(const void* A, int64_t base, int64_t k, in
 template <int DT>
 __device__ __forceinline__ void quant_pair_eal(const void* __restrict__ A, int64_t M, int64_t K, int64_t lda, int G,
                                                int64_t Mpad, uint8_t* __restrict__ acts, float* __restrict__ sa,
-                                               int32_t* __restrict__ asum, int32_t* err, int64_t m, int g, int lane) {
+                                               int32_t* __restrict__ asum, int32_t* err, int64_t m, int g, int lane,
+                                               int f16) {
     const int64_t b = int64_t(g) * 128;
     const int len = static_cast<int>(K - b < 128 ? K - b : 128);
     float x[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -87,7 +87,7 @@ __device__ __forceinline__ void quant_pair_eal(const void* __restrict__ A, int64
     int csum = 0;
     if (m < M) {
         if (!finite && lane == 0 && err) atomicMin(err, static_cast<int32_t>(m * G + g));
-        s = act_scale(amax, 0);
+        s = act_scale(amax, f16);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             if (4 * lane + i < len) {

@@ -48,6 +48,13 @@ __host__ __device__ inline uint32_t eal_offset(uint32_t m, uint32_t k) {
 // chunk boundaries. Items cut between CTAs are reduced by the piece that
 // completes their G groups (arrival counter counts groups).
 constexpr int kSkMax = 160;  // >= SMs of the device
+// Counter words at the start of every forward workspace, indexed by item (a
+// launch with split items has TB == 1, or fewer items than SMs) or by
+// stream-K boundary (<= kSkMax): a fixed region, so one workspace serves any M
+// and any layer. Every launch leaves the words it used at zero.
+constexpr int kCntWords = 8192;
+// per-token activation quantization (EAL row kernel): one CTA holds a whole row
+constexpr int64_t kPerTokenKMax = 32768;
 
 struct GemmParams {
     int32_t T8, T4;         // 128-row tiles of sub8 / sub4
@@ -73,9 +80,12 @@ struct GemmParams {
     int32_t lgS8, lgS4;     // log2 of S8 / S4: unit decoding uses shifts, not divisions
     int32_t units;          // work units (token block x tile x K-slice)
     int32_t grid;           // persistent CTAs (<= SMs): CTA b runs units b, b + grid, ...
-    float* part;            // split-K partial tiles [units][BN][128] (slot = unit index)
-    uint32_t* cnt;          // arrival counters [TB * (T8 + T4)], zero between launches
-    uint32_t* gen;          // per-item barrier generations [TB * (T8 + T4)] (any value)
+    float* part;            // split-K partial tiles [units][BN][128] (slot = unit index); stream-K: tails
+    float* part2;           // stream-K: head partial tiles [grid + 1][BN][128]
+    uint32_t* cnt;          // arrival counters [kCntWords] (item, or stream-K boundary), zero between launches
+    int32_t no_spin;        // 1: no cross-CTA spin-waits (concurrent launches may hold SMs)
+    const uint8_t* pf;      // next layer's packed weights: prefetched into L2 once this launch's reads are issued
+    int64_t pf_bytes;       // bytes of pf to prefetch (0: none), split evenly over the CTAs
     int32_t rotate;         // 1: each CTA starts its K loop at a CTA-dependent chunk (FAST modes)
     uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int32_t* partials;      // dump mode
@@ -137,8 +147,8 @@ cudaError_t launch_act_quant(const void* A, int a_dtype, int64_t M, int64_t K, i
 // writes asum [G][Mpad] int32 = the sum of each (group, token)'s codes, the
 // zero-point correction term of the decode GEMM (sum a(c - z) = sum a c - z sum a).
 cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t K, int64_t lda, int group,
-                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum, int32_t* err, bool pdl,
-                                 cudaStream_t stream);
+                                 int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum, int32_t* err, int f16,
+                                 bool pdl, cudaStream_t stream);
 // Row-major codes [M, ldc] + group-major scales [G, lds] (or [M]) -> EAL (+ asum).
 cudaError_t launch_repack_eal(const int8_t* codes, int64_t ldc, const float* scales, int64_t lds, int per_token,
                               int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum,

@@ -388,8 +388,14 @@ def _stream(stream):
 
 
 def exec_opts(mode: int = capi.MQ_EXACT, act_group: int = 0, ksplit: int = 0, token_tile: int = 0,
-              gemm_impl: int = 0, pdl: bool = True, schedule: int = 0) -> capi.mq_exec_opts:
-    return capi.mq_exec_opts(mode, act_group, ksplit, token_tile, gemm_impl, 0 if pdl else 1, schedule)
+              gemm_impl: int = 0, pdl: bool = True, schedule: int = 0, concurrent: bool = False,
+              act_scale_f16: bool = False, prefetch_next: "DeviceLayer | None" = None,
+              prefetch_bytes: int = 0) -> capi.mq_exec_opts:
+    """mq_exec_opts (capi.h). prefetch_next: the DeviceLayer this stream runs next
+    (its weights are prefetched into L2 at the end of this launch's reads)."""
+    return capi.mq_exec_opts(mode, act_group, ksplit, token_tile, gemm_impl, 0 if pdl else 1, schedule,
+                             int(concurrent), int(act_scale_f16),
+                             prefetch_next.h.value if prefetch_next is not None else None, prefetch_bytes)
 
 
 class DeviceLayer:
@@ -494,12 +500,22 @@ class DeviceLayer:
         return out
 
 
-def quantize_act(A, group_size: int, ldc: int | None = None, err=None, stream=None):
+def quantize_act(A, group_size: int, ldc: int | None = None, err=None, stream=None, scale_f16: bool = False):
     """Activation quantization on device: returns (codes int8 [M, ldc],
     scales f32 group-major [G, lds]; G = 1 for per-token). scales[:, :M].T is
-    the reference's [M, G] array."""
+    the reference's [M, G] array. scale_f16: the scheme's scale_f16_storage."""
     import torch
     M, K = A.shape
+    if scale_f16:
+        ldc = ldc or (K + 127) // 128 * 128
+        codes = torch.empty((M, ldc), dtype=torch.int8, device=A.device)
+        G = 1 if group_size >= K else (K + group_size - 1) // group_size
+        lds = (M + 3) // 4 * 4
+        scales = torch.empty((G, lds), dtype=torch.float32, device=A.device)
+        sc = capi.mq_scheme(8, 1, group_size, 1)
+        check(lib().mq_quantize_act_scheme(_p(A), _dt(A), M, K, A.stride(0), C.byref(sc), _p(codes), ldc,
+                                           _p(scales), lds, _p(err), _stream(stream)))
+        return codes, scales
     ldc = ldc or (K + 127) // 128 * 128
     codes = torch.empty((M, ldc), dtype=torch.int8, device=A.device)
     G = 1 if group_size >= K else (K + group_size - 1) // group_size
@@ -533,7 +549,8 @@ def execute_mixed_linear(activations: np.ndarray, layer: MixedLinearLayer, act_s
         raise UsageError("activation K does not match the layer's in_features")
     dl = DeviceLayer(layer, device, w8_mode)
     err = torch.full((1,), 2**31 - 1, dtype=torch.int32, device=f"cuda:{device}")
-    Y = dl.forward(torch.from_numpy(A).to(f"cuda:{device}"), opts=exec_opts(mode, act_scheme.group_size), err=err)
+    Y = dl.forward(torch.from_numpy(A).to(f"cuda:{device}"),
+                   opts=exec_opts(mode, act_scheme.group_size, act_scale_f16=act_scheme.scale_f16_storage), err=err)
     torch.cuda.synchronize(device)
     e = int(err.item())
     if e != 2**31 - 1:

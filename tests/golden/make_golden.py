@@ -33,6 +33,22 @@ CASES = [
     (33, 1024, 1024, 0.10),
 ]
 
+# The shapes bench.py measures (BASELINE configs[1] fused 8B projections) and the
+# Llama-3.1-70B linear shapes (configs[2]): exact-mode output checksums from the
+# reference's execute_mixed_linear (workers = nproc; the result does not depend
+# on workers, gemm.cpp:159-172 writes disjoint outputs).
+LARGE = [
+    (16, 6144, 4096, 0.10),    # 8B fused qkv
+    (16, 28672, 4096, 0.10),   # 8B fused gate_up
+    (16, 4096, 14336, 0.10),   # 8B down (G = 112)
+    (512, 4096, 14336, 0.10),  # 8B down, prefill
+    (16, 8192, 8192, 0.10),    # 70B q / o
+    (16, 1024, 8192, 0.10),    # 70B k / v
+    (1, 28672, 8192, 0.10),    # 70B gate / up
+    (16, 8192, 28672, 0.10),   # 70B down (G = 224)
+    (256, 8192, 8192, 0.10),   # 70B o, prefill
+]
+
 
 def main() -> None:
     O.build(ref=True)
@@ -54,6 +70,33 @@ def main() -> None:
                                  out_f32=O.fnv1a_hex(Y), ref_ms=rb["wall_ms"],
                                  out_first=[float(x) for x in Y.reshape(-1)[:4]]))
         print(out["cases"][-1])
+    out["cases_large"] = []
+    for m, n, k, p in LARGE:
+        W, A, prom = O.bench_inputs(m, n, k, p, 1)
+        R = O.RefLayer(W, prom, 128)
+        del W
+        Y, ms = R.forward(A, fast=True, workers=os.cpu_count() or 1)
+        codes = np.zeros((m, k), np.uint8)
+        scales = np.zeros((m, (k + 127) // 128), np.float32)
+        st = O.ref().mqref_quantize_tensor(O._ptr(A), 0, m, k, 8, 1, 128, 0, O._ptr(codes), O._ptr(scales), None)
+        assert st == 0
+        out["cases_large"].append(dict(m=m, n=n, k=k, percent=p, n8=R.n8, n4=R.n4,
+                                       act_codes=O.fnv1a_hex(codes), act_scales=O.fnv1a_hex(scales),
+                                       out_f32=O.fnv1a_hex(Y), ref_ms=ms,
+                                       out_first=[float(x) for x in Y.reshape(-1)[:4]]))
+        print(out["cases_large"][-1], flush=True)
+    # the activation scheme's scale_f16_storage (quant.hpp:70-76, quant.cpp:81-86):
+    # C1 inputs, activation scales rounded to binary16 by the reference
+    m, n, k, p = CASES[0]
+    W, A, prom = O.bench_inputs(m, n, k, p, 1)
+    R = O.RefLayer(W, prom, 128)
+    Y, _ = R.forward(A, fast=True, act_f16=True)
+    codes = np.zeros((m, k), np.uint8)
+    scales = np.zeros((m, (k + 127) // 128), np.float32)
+    assert O.ref().mqref_quantize_tensor(O._ptr(A), 0, m, k, 8, 1, 128, 1, O._ptr(codes), O._ptr(scales), None) == 0
+    out["act_f16"] = dict(m=m, n=n, k=k, percent=p, act_codes=O.fnv1a_hex(codes), act_scales=O.fnv1a_hex(scales),
+                          out_f32=O.fnv1a_hex(Y))
+    print(out["act_f16"], flush=True)
     # SPEC.md:428 hand example: A_q=[1,-2], s_a=0.1; codes [3,5] (0x53), z=4, s_w=0.5, g=2 -> -0.15
     out["spec_hand_example"] = {"expected": float(np.float32(-0.150000006))}
     with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json"), "w") as f:

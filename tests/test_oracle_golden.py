@@ -235,6 +235,28 @@ def test_oracle_reproduces_reference_checksums(golden, idx):
         assert Y.reshape(-1)[:4].tolist() == c["out_first"]
 
 
+def test_oracle_reproduces_reference_f16_activation_scales(golden):
+    """The activation scheme's scale_f16_storage (quant.hpp:70-76, quant.cpp:81-86):
+    codes, scales and output equal the reference's on the C1 inputs."""
+    c = golden["act_f16"]
+    W, A, prom = O.bench_inputs(c["m"], c["n"], c["k"], c["percent"], 1)
+    L = O.partition_and_quantize(W, prom)
+    Y, codes, scales = O.mixed_linear(L, A, act_f16=True)
+    assert O.fnv1a_hex(codes) == c["act_codes"] and O.fnv1a_hex(scales) == c["act_scales"]
+    assert O.fnv1a_hex(Y) == c["out_f32"]
+
+
+@pytest.mark.parametrize("idx", [0, 5])
+def test_oracle_reproduces_large_reference_checksums(golden, idx):
+    """Two of the bench-shape goldens (70B k/v 1024x8192 and the 8B fused qkv
+    6144x4096 at M = 16) through the oracle; the GPU checks all nine."""
+    c = golden["cases_large"][idx]
+    W, A, prom = O.bench_inputs(c["m"], c["n"], c["k"], c["percent"], 1)
+    L = O.partition_and_quantize(W, prom)
+    Y, codes, scales = O.mixed_linear(L, A)
+    assert O.fnv1a_hex(codes) == c["act_codes"] and O.fnv1a_hex(Y) == c["out_f32"]
+
+
 # --------------------------------------- 4. oracle vs the reference build
 needs_ref = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (needs /root/reference)")
 
