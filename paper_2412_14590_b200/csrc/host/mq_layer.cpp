@@ -36,6 +36,7 @@ struct mq_layer_s {
     int64_t tiles8 = 0, tiles4 = 0;
     int split4[3] = {1, 1, 1};          // K-split chosen once at create (choose_split) for token
     int split8[3] = {1, 1, 1};          // tiles <= 32 (decode), 64 and 128 (one token block)
+    double split_span[3] = {0, 0, 0};   // the chosen split's modelled busiest-CTA cost (sub4 groups)
     uint8_t* d_wq = nullptr;
     int32_t* d_colmap = nullptr;
     int64_t bytes_wq = 0, stream_bytes = 0;
@@ -96,6 +97,15 @@ bool stream_k_pays(const mq_layer_s* L, const Plan* pl, bool force) {
     return per_cta + cut_cost < double(rounds * G);
 }
 
+// Decode (token tiles <= 32, one token block) stream-K: every CTA streams the
+// same bytes (a sub8 group costs two sub4 groups); an item cut across CTAs is
+// joined by its last piece (any number of pieces, see the kernel). Measured on
+// the Llama decode shapes it loses to the unit schedule even where it balances
+// better (gate_up 28672x4096: 21.9 vs 18.6 us): a join in the middle of a
+// CTA's range stalls its epilogue, and decode is bound by the per-SM pipeline.
+// So the unit schedule stays the default and schedule = 2 forces stream-K.
+bool decode_stream_k_pays(const mq_layer_s*, bool force) { return force; }
+
 void plan_stream_k(const mq_layer_s* L, Plan* pl) {
     const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4, T = T8 + T4;
     const int64_t c8 = pl->bn <= 32 ? 2 : 1;
@@ -121,7 +131,11 @@ void plan_stream_k(const mq_layer_s* L, Plan* pl) {
         pl->skb[b] = static_cast<uint32_t>(((tb * T + t) << 8) | g);
     }
     pl->skb[grid] = static_cast<uint32_t>((int64_t(pl->tb) * T) << 8);
-    pl->grid = grid;
+    // chunk rounding can make neighbouring boundaries equal: drop the empty
+    // ranges, so the boundaries are strictly increasing (the decode join finds
+    // an item's pieces as the CTAs between two boundary searches)
+    pl->skb.erase(std::unique(pl->skb.begin(), pl->skb.end()), pl->skb.end());
+    pl->grid = static_cast<int>(pl->skb.size()) - 1;
     pl->sk = true;
 }
 
@@ -158,6 +172,7 @@ void best_split(mq_layer_s* L, int kind) {
                 best = span;
                 L->split4[kind] = S4;
                 L->split8[kind] = S8;
+                L->split_span[kind] = span;
             }
         }
     }
@@ -249,6 +264,9 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
         items * 256 < (int64_t(1) << 32) &&
         o->schedule != 1 && stream_k_pays(L, pl, o->schedule == 2))
         plan_stream_k(L, pl);
+    if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn <= 32 && pl->tb == 1 && L->G < 256 && o->schedule != 1 &&
+        decode_stream_k_pays(L, o->schedule == 2))
+        plan_stream_k(L, pl);
     static const bool plan_log = std::getenv("MQ_PLAN_LOG") != nullptr;  // development
     if (plan_log)
         std::fprintf(stderr, "mq plan: N=%lld K=%lld M=%lld bn=%d tb=%d S4=%d S8=%d units=%d grid=%d sk=%d\n",
@@ -276,10 +294,12 @@ EalWs eal_ws_layout(const mq_layer_s* L, const Plan& pl) {
     w.off_part = w.off_asum + al(size_t(L->G) * size_t(pl.Mpad) * 4);
     const bool split = pl.S4 > 1 || pl.S8 > 1;
     const size_t tile = 128 * size_t(pl.bn) * 4;
+    // decode stream-K: two slots per CTA (its first and last piece); prefill
     // stream-K: tail partials [grid + 1] then head partials [grid + 1]
-    const size_t slots = pl.sk ? size_t(pl.grid) + 1 : split ? size_t(pl.units) : 0;
+    const size_t slots = pl.sk ? (pl.bn <= 32 ? 2 * (size_t(pl.grid) + 1) : size_t(pl.grid) + 1)
+                               : split ? size_t(pl.units) : 0;
     w.off_part2 = w.off_part + al(slots * tile);
-    w.total = w.off_part2 + (pl.sk ? al(slots * tile) : 0);
+    w.total = w.off_part2 + (pl.sk && pl.bn > 32 ? al(slots * tile) : 0);
     return w;
 }
 

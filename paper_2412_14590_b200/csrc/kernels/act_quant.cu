@@ -264,12 +264,14 @@ cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t 
 #undef MQ_ROWS
 #undef MQ_ROW
     }
+    // 4 warps per CTA: a small footprint, so the CTAs fit beside two decode K2
+    // CTAs on an SM (the launch before and the launch after, mixed_gemm_sm100.cu)
     const int64_t warps = Mpad * G;
-    const dim3 grid(static_cast<unsigned>((warps * 32 + 255) / 256));
+    const dim3 grid(static_cast<unsigned>((warps * 32 + 127) / 128));
     switch (a_dtype) {
-        case 0: return launch_ex(act_quant_eal_group_kernel<0>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
-        case 1: return launch_ex(act_quant_eal_group_kernel<1>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
-        default: return launch_ex(act_quant_eal_group_kernel<2>, grid, dim3(256), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
+        case 0: return launch_ex(act_quant_eal_group_kernel<0>, grid, dim3(128), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
+        case 1: return launch_ex(act_quant_eal_group_kernel<1>, grid, dim3(128), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
+        default: return launch_ex(act_quant_eal_group_kernel<2>, grid, dim3(128), pdl, stream, A, M, K, lda, G, Mpad, acts, sa, asum, err, f16);
     }
 }
 

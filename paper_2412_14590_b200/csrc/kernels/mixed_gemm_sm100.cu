@@ -49,6 +49,18 @@ constexpr int kSmemMax = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 
 template <int BN>
 struct TcCfg {
+    // Decode token tiles (<= 32 tokens) size a CTA for TWO per SM (half the
+    // shared memory, registers and TMEM): the next launch's CTAs then become
+    // resident while this launch's CTAs finish (split-K join, scattered output
+    // stores), so under PDL the next projection's weights stream into its
+    // rings during this one's tail. Token-tiled (prefill) launches own the SM.
+#ifndef MQ_DEC2
+#define MQ_DEC2 0
+#endif
+    static constexpr bool kDec = MQ_DEC2 && BN <= 32;
+    static constexpr int kMinBlocks = kDec ? 2 : 1;
+    static constexpr int kSmemBudget = kDec ? 113 * 1024 : kSmemMax;
+    static constexpr uint32_t kTmemBudget = kDec ? 256u : 512u;
     static constexpr int GPS = gemm_gps(BN);                // sub4 groups per chunk
     static constexpr int GPS8 = GPS / 2 > 0 ? GPS / 2 : 1;  // sub8 groups per chunk
     static constexpr int kRaw0 = GPS * kBlock4Bytes > GPS8 * kBlock8Bytes ? GPS * kBlock4Bytes : GPS8 * kBlock8Bytes;
@@ -65,18 +77,18 @@ struct TcCfg {
     static constexpr int kXStageBytes = ((kOffAs + (kZpEpi ? GPS * BN * 4 : 0)) + 1023) / 1024 * 1024;
     // activation stages: a prefill tile needs a fresh 16 KB activation tile per
     // group (from L2), so its ring is as deep as the weight ring
-    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? 6 : 3;
-    // TMEM rings (512 columns): NT accumulator chunk slots of GPS x BN int32
-    // columns, NA A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
+    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? 6 : (kDec && BN == 16) ? 4 : 3;
+    // TMEM rings: NT accumulator chunk slots of GPS x BN int32 columns, NA
+    // A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
     static constexpr int NT = BN >= 128 ? 3 : 2;
-    static constexpr int NA0 = int((512u - NT * kAccPerChunk) / kAPerChunk);
+    static constexpr int NA0 = int((kTmemBudget - NT * kAccPerChunk) / kAPerChunk);
     static constexpr int NA = NA0 > 4 ? 4 : NA0;
     static constexpr uint32_t kAccCols = NT * kAccPerChunk;
     static constexpr uint32_t kACol0 = kAccCols;
     static constexpr uint32_t kTmemNeed = kAccCols + NA * kAPerChunk;
     static constexpr uint32_t kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
-    static_assert(kTmemNeed <= 512 && NA >= 2, "TMEM budget");
+    static_assert(kTmemCols <= kTmemBudget && NA >= 2, "TMEM budget");
     // meta ring (per accumulator slot): weight scales [GPS][128] | (kZpEpi) zero
     // points [GPS][128] | act scales [GPS][BN] | (kZpEpi) code sums [GPS][BN]
     static constexpr int kMetaZp = GPS * 128, kMetaSa = GPS * 128 * (kZpEpi ? 2 : 1), kMetaAs = kMetaSa + GPS * BN;
@@ -86,24 +98,30 @@ struct TcCfg {
     static constexpr int NM = 4;
     static constexpr int kMetaBytes = NM * kMetaSlot;
     static constexpr int kFixed = 1024 /*alignment slack*/ + 1024 /*barriers*/ + kMetaBytes + NX * kXStageBytes;
-    static constexpr int NS0 = (kSmemMax - kFixed) / kStageBytes;
+    static constexpr int NS0 = (kSmemBudget - kFixed) / kStageBytes;
 #ifndef MQ_NS_MAX
 #define MQ_NS_MAX 8
 #endif
     static constexpr int NS = NS0 > MQ_NS_MAX ? MQ_NS_MAX : NS0;
-    // epilogue warpgroups: two (one at BN = 64, where a second measured ~2%
-    // slower) — one warp per SMSP leaves the TMEM-load / rescale chain
-    // latency-bound (A/B at 32-token tiles: 6-18% faster with two)
-    static constexpr int NE = BN == 64 ? 1 : 2;
-    // converter warpgroups: two at 16-token tiles (conversion-bound); from 32
-    // tokens the rescale dominates and one warpgroup converts fast enough
-    // (A/B: 32-token launches 6-23% faster with one)
-    static constexpr int NC = BN == 16 ? 2 : 1;
+    // epilogue warpgroups: two for 128-token tiles (one warp per SMSP leaves
+    // the TMEM-load / rescale chain latency-bound), one at 64 tokens (a second
+    // measured ~2% slower) and at decode (two CTAs per SM share the SMSPs)
+    #ifndef MQ_NE16
+#define MQ_NE16 2
+#endif
+#ifndef MQ_NC16
+#define MQ_NC16 2
+#endif
+    static constexpr int NE = BN == 16 ? (kDec ? 1 : MQ_NE16) : (BN == 64 || kDec) ? 1 : 2;
+    // converter warpgroups: one (at decode the two co-resident CTAs provide the
+    // second; from 32 tokens the rescale dominates)
+    static constexpr int NC = (BN == 16 && !kDec) ? MQ_NC16 : 1;
     static constexpr int BNE = BN / NE;          // tokens per epilogue warpgroup
     static constexpr int kEpiThread0 = 128 * (1 + NC);
     static constexpr int kThreads = 128 * (1 + NC + NE);
     static constexpr int kSmem = kFixed + NS * kStageBytes;
     static_assert(NS >= 2, "pipeline needs at least two stages");
+    static_assert(kSmem <= kSmemBudget, "shared memory budget");
     static_assert(GPS * BN <= 128, "act-scale copy: one converter thread per value");
 };
 
@@ -184,6 +202,18 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
 __device__ __forceinline__ void unpack_word(uint32_t w, uint32_t kk, uint32_t& lo, uint32_t& hi) {
     lo = ((w & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
     hi = (((w >> 4) & 0x0F0F0F0Fu) + kk) ^ 0x80808080u;
+}
+
+// Stream-K: the CTA whose range [skb[b], skb[b+1]) holds position `key`
+// (item << 8 | group); the plan's boundaries are strictly increasing.
+__device__ __forceinline__ int sk_cta_of(const GemmParams& p, uint32_t key) {
+    int lo = 0, hi = p.grid - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p.skb[mid] <= key) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
 }
 
 // Stream-K split piece epilogue. Every CTA's range covers at least one item's
@@ -336,7 +366,7 @@ __device__ __noinline__ void split_join_wide(const GemmParams& p, const Work& wk
 // unit schedules of 64/128-token tiles; its out-of-line call costs the other
 // wide launches ~4% in the accumulation loop's register allocation)
 template <int BN, int MODE, int SPL>
-__global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(const __grid_constant__ GemmParams p) {
+__global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mixed_gemm_tc_kernel(const __grid_constant__ GemmParams p) {
     using C = TcCfg<BN>;
     constexpr int NS = C::NS, NE = C::NE, BNE = C::BNE, GPS = C::GPS, NA = C::NA, NT = C::NT, NC = C::NC;
     constexpr bool kSa = (MODE == kExactGroup || MODE == kFastGroup);
@@ -391,7 +421,10 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         ptx::fence_barrier_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) trace(p, 0);
+    if (threadIdx.x == 0) {
+        trace(p, 0);
+        trace_chunk(p, 14, 0);
+    }
     griddep_launch();  // let the next kernel in the stream start its prologue
 
     // Persistent: CTA b walks work units b, b + grid, b + 2 grid, ... (each unit
@@ -455,7 +488,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
     if (warp == 0) {
         // ============================== producer ==============================
         if (lane == 0) trace(p, 2);
+        if (lane == 0) trace_chunk(p, 15, 1);
         const uint64_t pol_w = ptx::policy_evict_first();
+        if (lane == 0) trace_chunk(p, 15, 2);
         // weights are immutable: this warp never waits on the previous kernel
         // (griddepcontrol), so under PDL the first NS stages fill while it runs
         Ring rr;
@@ -463,11 +498,14 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         for (int pk = 0;; ++pk) {
             Unit U;
             if (!piece(pk, U)) break;
+            if (lane == 0 && pk == 0) trace_chunk(p, 15, 3);
             for (int i = 0; i < U.nch; ++i, ++n) {
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
                 uint8_t* st = stage(rr.idx);
+                if (lane == 0 && n == 0) trace_chunk(p, 15, 4);
                 ptx::mbar_wait(&empty[rr.idx], rr.ph ^ 1u);
+                if (lane == 0 && n == 0) trace_chunk(p, 15, 5);
                 if (lane == 0) trace_chunk(p, 0, n);
                 if (n == 0 && lane == 0) trace(p, 7);
                 const uint32_t wbytes = uint32_t(cg * U.ti.blk);
@@ -897,12 +935,22 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                 }
                 continue;
             }
-            // split-K (decode token tiles only): publish this slice's partial tile
-            // [128][BN] (slot = unit; a thread's tokens are contiguous -> float4),
-            // count arrivals; the last slice sums all S partials in slice order
-            // (deterministic) and scatters them
+            // split item at decode (token tiles <= 32): publish this piece's
+            // partial tile [128][BN] (a thread's tokens are contiguous -> float4),
+            // count arrivals; the last piece sums all S partials in piece order
+            // (deterministic) and scatters them. Unit schedule: the item's slices
+            // are units cta0 .. cta0 + S - 1 (slot = unit). Decode stream-K: the
+            // item's pieces lie on consecutive CTAs b_f .. b_l; CTA b's first
+            // piece uses slot 2b, its last (a head cut at the range end) 2b + 1.
             if constexpr (BN <= 32) {
-            float4* mine = reinterpret_cast<float4*>(p.part + int64_t(U.key) * (BN * 128) + r * BN + c0);
+            int S = wk.S, my = U.key, b_f = wk.cta0;
+            if (p.sk) {
+                b_f = sk_cta_of(p, uint32_t(wk.item) << 8);
+                S = sk_cta_of(p, (uint32_t(wk.item) << 8) | uint32_t(p.G - 1)) - b_f + 1;
+                my = 2 * int(blockIdx.x) + (pk == 0 ? 0 : 1);
+            }
+            if (et == 0) trace_chunk(p, 11, n);
+            float4* mine = reinterpret_cast<float4*>(p.part + int64_t(my) * (BN * 128) + r * BN + c0);
 #pragma unroll
             for (int j = 0; j < BNE / 4; ++j)
                 __stcg(mine + j, make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]));
@@ -910,31 +958,39 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
             if (et == 0) {
                 // release: this CTA's partial (ordered before by bar.sync) is
                 // visible at gpu scope before the count; acquire: the other
-                // slices' partials are visible to the reduction below (ordered
+                // pieces' partials are visible to the reduction below (ordered
                 // after by bar.sync; ld.cg reads L2) — no full fences
                 uint32_t prev;
                 asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.cnt + wk.item) : "memory");
-                *s_last = prev == uint32_t(wk.S - 1);
-                if (prev == uint32_t(wk.S - 1)) p.cnt[wk.item] = 0u;  // re-arm for the next launch
+                *s_last = prev == uint32_t(S - 1);
+                if (prev == uint32_t(S - 1)) p.cnt[wk.item] = 0u;  // re-arm for the next launch
             }
             named_bar_sync(2, 128 * NE);
             const bool last = *s_last != 0;
             named_bar_sync(2, 128 * NE);  // s_last is reused by the next unit
+            if (et == 0) trace_chunk(p, 12, n);
             if (last) {
-                const float4* base = reinterpret_cast<const float4*>(p.part + int64_t(wk.cta0) * (BN * 128) + r * BN + c0);
-                constexpr int V = BNE / 4;              // float4s per slice
-                constexpr int SB = 32 / BNE;            // slices per batch: every load of a batch in flight
+                // slot of piece j of the item (in order)
+                const bool first_own = p.sk && (p.skb[b_f] >> 8) == uint32_t(wk.item);
+                auto slot_of = [&](int j) -> int64_t {
+                    if (!p.sk) return int64_t(b_f) + j;
+                    return int64_t(2 * (b_f + j)) + ((j == 0 && !first_own) ? 1 : 0);
+                };
+                constexpr int V = BNE / 4;      // float4s per piece
+                constexpr int SB = 32 / BNE;    // pieces per batch: every load of a batch in flight
                 float sum[BNE];
-                for (int s0 = 0; s0 < wk.S; s0 += SB) {
+                for (int s0 = 0; s0 < S; s0 += SB) {
                     float4 t[SB][V];
 #pragma unroll
                     for (int s2 = 0; s2 < SB; ++s2)
-                        if (s0 + s2 < wk.S)
+                        if (s0 + s2 < S) {
+                            const float4* src = reinterpret_cast<const float4*>(p.part + slot_of(s0 + s2) * (BN * 128) + r * BN + c0);
 #pragma unroll
-                            for (int q = 0; q < V; ++q) t[s2][q] = __ldcg(base + int64_t(s0 + s2) * (BN * 32) + q);
+                            for (int q = 0; q < V; ++q) t[s2][q] = __ldcg(src + q);
+                        }
 #pragma unroll
                     for (int s2 = 0; s2 < SB; ++s2) {
-                        if (s0 + s2 >= wk.S) break;
+                        if (s0 + s2 >= S) break;
 #pragma unroll
                         for (int q = 0; q < V; ++q) {
                             const float tv[4] = {t[s2][q].x, t[s2][q].y, t[s2][q].z, t[s2][q].w};
@@ -944,6 +1000,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
                         }
                     }
                 }
+                if (et == 0) trace_chunk(p, 15, 8);
                 if (col >= 0) {
 #pragma unroll
                     for (int j = 0; j < BNE; ++j) {
@@ -960,7 +1017,10 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, 1) mixed_gemm_tc_kernel(c
         }
     }
 
-    if (threadIdx.x == C::kEpiThread0) trace(p, 5);
+    if (threadIdx.x == C::kEpiThread0) {
+        trace(p, 5);
+        trace_chunk(p, 15, 0);
+    }
     ptx::tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) trace(p, 6);

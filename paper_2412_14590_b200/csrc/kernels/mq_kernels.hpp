@@ -57,44 +57,47 @@ constexpr int kCntWords = 8192;
 constexpr int64_t kPerTokenKMax = 32768;
 
 struct GemmParams {
+    // Hot fields first: every role decodes its first unit from these before its
+    // first chunk, so they share one 64-byte constant-cache line (cold param
+    // lines cost a dependent constant-bank miss each at kernel start).
+    int32_t sk;             // 1: stream-K schedule (skb), 0: unit schedule (units/S8/S4)
+    int32_t units;          // work units (token block x tile x K-slice)
     int32_t T8, T4;         // 128-row tiles of sub8 / sub4
-    int64_t n8, n4;         // rows of sub8 / sub4
-    int32_t G;              // K-groups
     int32_t TB;             // token blocks (BN tokens each)
-    int64_t K;
+    int32_t G;              // K-groups
+    int32_t S8, S4;         // K-slices per sub8 / sub4 item (powers of two)
+    int32_t lgS8, lgS4;     // log2 of S8 / S4: unit decoding uses shifts, not divisions
+    int32_t rotate;         // 1: each CTA starts its K loop at a CTA-dependent chunk (FAST modes)
+    int32_t T;              // T8 + T4
+    int32_t dbg;            // development: pipeline-stage bypass bits (MQ_DBG env), 0 in production
+    int32_t grid;           // persistent CTAs (<= SMs): CTA b runs units b, b + grid, ...
     const uint8_t* wq;      // merged code+meta blocks (mq_layout.cuh)
+    int64_t n8, n4;         // rows of sub8 / sub4
     const int32_t* colmap;  // [ (T8+T4)*128 ] output column of every tile row
     // EAL activations (tensor-core kernel)
     const uint8_t* acts;    // [G][Mpad][128]
     const float* sa;        // [G][Mpad] (group-wise) or [Mpad] (per-token)
     const int32_t* asum;    // [G][Mpad] per-(group, token) code sums (zero-point correction)
     int64_t Mpad;
+    int64_t M;
+    unsigned long long* trace;  // development: per-CTA globaltimer stamps [P][8] (MQ_DBG & 32)
+    int64_t K;
     // row-major activations (SIMT debug kernel): scales sa_rm[g * sa_gstride + m]
     const float* sa_rm;
     int64_t sa_gstride;
-    int64_t M;
     void* Y;
     int32_t out_dtype;      // mq_dtype
+    uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int64_t ldy;
-    int32_t S8, S4;         // K-slices per sub8 / sub4 item (powers of two)
-    int32_t lgS8, lgS4;     // log2 of S8 / S4: unit decoding uses shifts, not divisions
-    int32_t units;          // work units (token block x tile x K-slice)
-    int32_t grid;           // persistent CTAs (<= SMs): CTA b runs units b, b + grid, ...
     float* part;            // split-K partial tiles [units][BN][128] (slot = unit index); stream-K: tails
     float* part2;           // stream-K: head partial tiles [grid + 1][BN][128]
     uint32_t* cnt;          // arrival counters [kCntWords] (item, or stream-K boundary), zero between launches
     int32_t no_spin;        // 1: no cross-CTA spin-waits (concurrent launches may hold SMs)
+    int32_t partial_rows;
     const uint8_t* pf;      // next layer's packed weights: prefetched into L2 once this launch's reads are issued
     int64_t pf_bytes;       // bytes of pf to prefetch (0: none), split evenly over the CTAs
-    int32_t rotate;         // 1: each CTA starts its K loop at a CTA-dependent chunk (FAST modes)
-    uint32_t idesc8;        // instruction descriptor bits for sub8 tiles (u8 or s8 A)
     int32_t* partials;      // dump mode
-    int32_t partial_rows;
-    int32_t sk;             // 1: stream-K schedule (skb), 0: unit schedule (units/S8/S4)
-    int32_t T;              // T8 + T4
     uint32_t skb[kSkMax + 1];  // stream-K CTA boundaries (item << 8 | group)
-    int32_t dbg;            // development: pipeline-stage bypass bits (MQ_DBG env), 0 in production
-    unsigned long long* trace;  // development: per-CTA globaltimer stamps [P][8] (MQ_DBG & 32)
 };
 
 // One unit's work: rows of `tile` x tokens of block `tb` x groups [g0, g1);

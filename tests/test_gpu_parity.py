@@ -321,3 +321,25 @@ def test_bf16_output_wide_split(cuda):
     y32 = dl.forward(dA, opts=o).cpu()
     y16 = dl.forward(dA, opts=o, out_dtype=torch.bfloat16).cpu()
     assert torch.equal(y16.float(), y32.to(torch.bfloat16).float())
+
+
+@pytest.mark.parametrize("m,n,k,sched,ag", [(16, 4096, 4096, 2, 128), (1, 4096, 4096, 2, 128), (16, 28672, 4096, 0, 128),
+                                            (32, 6144, 4096, 2, 128), (16, 4096, 14336, 2, 128),
+                                            (16, 4096, 4096, 2, 4096), (7, 640, 1000, 2, 128)])
+def test_fast_mode_decode_stream_k(cuda, m, n, k, sched, ag):
+    """Decode stream-K (token tiles <= 32): equal bytes per CTA, items cut into
+    any number of pieces on consecutive CTAs and joined by the last piece in
+    CTA order — within tolerance, bit-reproducible, and equal to the unit
+    schedule within tolerance. Covers per-token scales and a ragged K-group."""
+    import torch
+    L, A = _layer(m, n, k, 0.1, seed=47)
+    dl = mq.DeviceLayer(L)
+    dA = torch.from_numpy(A).to(cuda)
+    o = mq.exec_opts(capi.MQ_FAST, ag, schedule=sched)
+    Y = dl.forward(dA, opts=o).cpu().numpy()
+    ref, _, _ = O.mixed_linear(_oracle_layer(L), A, act_group=None if ag == 128 else ag)
+    assert _rel(Y, ref) <= TOL
+    for _ in range(2):
+        assert np.array_equal(dl.forward(dA, opts=o).cpu().numpy(), Y)
+    Yu = dl.forward(dA, opts=mq.exec_opts(capi.MQ_FAST, ag, schedule=1)).cpu().numpy()
+    assert _rel(Yu, ref) <= TOL

@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(512, 1) bulk_ring(const uint8_t* __restrict__ 
 }
 
 int main() {
+    setvbuf(stdout, NULL, _IONBF, 0);
     const size_t total = size_t(2) << 30;
     uint8_t* buf;
     cudaMalloc(&buf, total);
@@ -68,14 +69,15 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int mb : {1, 10, 35}) {
-        for (int hold : {0, 1}) {
+    for (int mb : {10, 35, 70}) {
+        for (int hold : {0}) {
           for (int big : {0, 1}) {
             const int ctas = 148, pdl = 1;
             {
-                const int chunk = 32768, depth = 6;
+              for (int cd : {0, 1, 2}) {
+                const int chunk = cd == 0 ? 32768 : cd == 1 ? 16384 : 8192, depth = cd == 0 ? 6 : cd == 1 ? 12 : 24;
                 const size_t per = std::max<size_t>(chunk, (size_t(mb) << 20) / ctas / chunk * chunk);
-                const int smem = big ? 232448 : chunk * depth + 1024;
+                const int smem = big ? 232448 : chunk * depth + 1024 + 512;
                 cudaFuncSetAttribute(bulk_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
                 const int nl = 20;
                 const size_t stride = per * ctas;
@@ -108,10 +110,11 @@ int main() {
                 float ms;
                 cudaEventElapsedTime(&ms, e0, e1);
                 const double us = ms * 1e3 / nl;
-                printf("graph stream %4d MB/launch hold=%d smem=%d: %7.2f us/launch  %6.0f GB/s\n", mb, hold, smem, us,
+                printf("graph stream %4d MB/launch chunk=%5d depth=%2d hold=%d smem=%6d: %7.2f us/launch  %6.0f GB/s\n", mb, chunk, depth, hold, smem, us,
                        double(per * ctas) / us / 1e3);
                 cudaGraphExecDestroy(ge);
                 cudaGraphDestroy(g);
+              }
             }
           }
         }

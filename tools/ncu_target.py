@@ -17,7 +17,7 @@ L = mq.partition_and_quantize(W, prom)
 dl = mq.DeviceLayer(L)
 dA = torch.from_numpy(A).cuda()
 Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
-opts = mq.exec_opts(mode, ag)
+opts = mq.exec_opts(mode, ag, ksplit=int(os.environ.get("KSPLIT", "0")))
 for _ in range(5):
     dl.forward(dA, out=Y, opts=opts)
 torch.cuda.synchronize()
