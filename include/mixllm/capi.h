@@ -169,6 +169,41 @@ typedef struct {
 } mq_layer_info;
 mq_status mq_layer_get_info(mq_layer_t layer, mq_layer_info* info);
 
+/* ===================================================================== */
+/* Offline quantization and prepack on the GPU        */
+/* ===================================================================== */
+
+/* partition_and_quantize (proj/src/mixed.cpp:46-81) on the GPU, bit-exact with
+ * mq_partition_and_quantize: W is a DEVICE f64 [N, K] row-major matrix,
+ * promoted a HOST list of output channels. The row gather and
+ * quantize_group_{sym,asym}<double> (quant.hpp:84-140) run as one kernel per
+ * sub-problem (a warp per (row, group), IEEE double throughout). The reference
+ * layouts are kept in device memory, owned by the returned handle; errors
+ * (non-finite input -> MQ_DATA with the first failing row/group, sub8 first)
+ * are reported before returning, like the reference's DataError. Synchronous
+ * w.r.t. `stream`. */
+typedef struct mq_device_qlayer_s* mq_device_qlayer_t;
+mq_status mq_partition_and_quantize_device(const double* W, int64_t N, int64_t K,
+                                           const int32_t* promoted, int64_t n_promoted,
+                                           const mq_scheme* largebit, const mq_scheme* smallbit,
+                                           int device, void* stream, mq_device_qlayer_t* out);
+/* Descriptor of a device-quantized layer: index maps are HOST pointers,
+ * payloads / scales / zero points DEVICE pointers (valid until destroy). */
+mq_status mq_device_qlayer_desc(mq_device_qlayer_t layer, mq_layer_desc* desc);
+void mq_device_qlayer_destroy(mq_device_qlayer_t layer);
+
+/* mq_layer_create from reference layouts already in device memory (desc:
+ * HOST index maps, DEVICE payload8 / scales8 / payload4 / scales4 /
+ * zero_points4, e.g. from mq_device_qlayer_desc): the engine layout is packed
+ * on the GPU (same bytes as the host packer). validate_quantized's scale and
+ * zero-point checks run on the device; synchronous w.r.t. `stream`. */
+mq_status mq_layer_create_device(const mq_layer_desc* desc, const mq_layer_opts* opts, int device,
+                                 void* stream, mq_layer_t* out);
+
+/* Parity / debugging: copy a layer's packed device layout (device_bytes bytes)
+ * and its tile-row column map ((tiles8 + tiles4) * 128 int32, nullable) to host. */
+mq_status mq_layer_export_packed(mq_layer_t layer, void* wq_host, size_t bytes, int32_t* colmap_host);
+
 /* Gather-order column map of a sharded layer: out[r*shard_cols + j] = original
  * output column of rank r's local column j, or -1 for padding. [world*shard_cols]. */
 mq_status mq_layer_shard_colmap(mq_layer_t layer, int32_t* out);

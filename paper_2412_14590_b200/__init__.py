@@ -9,6 +9,7 @@ from .mixquant import (  # noqa: F401
     SMALLBIT,
     DataError,
     DeviceLayer,
+    DeviceQuantizedLayer,
     MixedLinearLayer,
     QuantizedModel,
     QuantizedTensor,
@@ -23,6 +24,7 @@ from .mixquant import (  # noqa: F401
     fnv1a_hex,
     pack_nibbles,
     partition_and_quantize,
+    partition_and_quantize_device,
     permute_gathered,
     prepack_weights,
     quantize_act,

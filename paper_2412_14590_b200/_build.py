@@ -23,7 +23,8 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INC = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + os.path.join(CUDA, "include")]
 
-CU_SRCS = ["kernels/act_quant.cu", "kernels/mixed_gemm_sm100.cu", "kernels/mixed_gemm_simt.cu"]
+CU_SRCS = ["kernels/act_quant.cu", "kernels/mixed_gemm_sm100.cu", "kernels/mixed_gemm_simt.cu",
+           "kernels/weight_quant.cu"]
 CPP_SRCS = ["host/mq_host.cpp", "host/mq_layer.cpp"]
 
 

@@ -88,6 +88,13 @@ PROTOTYPES = {
     "mq_quantize_act_ws": (C.c_int, [P, P, C.c_int, I64, C.POINTER(mq_exec_opts), P, P, P]),
     "mq_mixed_linear_ws": (C.c_int, [P, I64, P, P, C.c_int, C.POINTER(mq_exec_opts), P]),
     "mq_permute_gathered": (C.c_int, [P, P, I32, I64, I64, I64, P, C.c_int, P]),
+    "mq_partition_and_quantize_device": (C.c_int, [P, I64, I64, P, I64, C.POINTER(mq_scheme), C.POINTER(mq_scheme),
+                                                   C.c_int, P, C.POINTER(P)]),
+    "mq_device_qlayer_desc": (C.c_int, [P, C.POINTER(mq_layer_desc)]),
+    "mq_device_qlayer_destroy": (None, [P]),
+    "mq_layer_create_device": (C.c_int, [C.POINTER(mq_layer_desc), C.POINTER(mq_layer_opts), C.c_int, P,
+                                         C.POINTER(P)]),
+    "mq_layer_export_packed": (C.c_int, [P, P, C.c_size_t, P]),
 }
 
 _lib = None

@@ -200,6 +200,25 @@ mq_status partition_maps(int64_t N, const int32_t* promoted, int64_t np,
 
 // mixed.cpp:14-44 + quant.cpp:81-101 on a descriptor.
 mq_status validate_desc(const mq_layer_desc* d) {
+    if (mq_status st = validate_maps(d)) return st;
+    const int64_t G = num_groups(d->in_features, d->group_size);
+    auto positive = [&](const float* s, int64_t n) {
+        for (int64_t i = 0; i < n; ++i)
+            if (!(s[i] > 0.0f)) return false;
+        return true;
+    };
+    if (d->n8 > 0 && !positive(d->scales8, d->n8 * G))
+        return fail(MQ_DATA, "quantized tensor has a non-positive scale");
+    if (d->n4 > 0 && !positive(d->scales4, d->n4 * G))
+        return fail(MQ_DATA, "quantized tensor has a non-positive scale");
+    if (d->n4 > 0)
+        for (int64_t i = 0; i < d->n4 * G; ++i)
+            if (d->zero_points4[i] > 15) return fail(MQ_DATA, "4-bit zero point out of [0, 15]");
+    return MQ_OK;
+}
+
+// mixed.cpp:14-44: shapes and index maps (host), payload pointers present.
+mq_status validate_maps(const mq_layer_desc* d) {
     if (!d) return fail(MQ_USAGE, "layer descriptor is null");
     if (d->out_features < 0 || d->in_features < 0 || d->n8 < 0 || d->n4 < 0)
         return fail(MQ_DATA, "mixed layer has a negative shape");
@@ -221,23 +240,10 @@ mq_status validate_desc(const mq_layer_desc* d) {
         if (seen[ch] != 1)
             return fail(MQ_DATA, "mixed layer: output channel " + std::to_string(ch) +
                                      (seen[ch] == 0 ? " is unassigned" : " is assigned twice"));
-    const int64_t G = num_groups(d->in_features, d->group_size);
-    auto positive = [&](const float* s, int64_t n) {
-        for (int64_t i = 0; i < n; ++i)
-            if (!(s[i] > 0.0f)) return false;
-        return true;
-    };
     if (d->n8 > 0 && (!d->payload8 || !d->scales8))
         return fail(MQ_DATA, "mixed layer: sub8 payload/scales missing");
     if (d->n4 > 0 && (!d->payload4 || !d->scales4 || !d->zero_points4))
         return fail(MQ_DATA, "asymmetric quantized tensor is missing zero points");
-    if (d->n8 > 0 && !positive(d->scales8, d->n8 * G))
-        return fail(MQ_DATA, "quantized tensor has a non-positive scale");
-    if (d->n4 > 0 && !positive(d->scales4, d->n4 * G))
-        return fail(MQ_DATA, "quantized tensor has a non-positive scale");
-    if (d->n4 > 0)
-        for (int64_t i = 0; i < d->n4 * G; ++i)
-            if (d->zero_points4[i] > 15) return fail(MQ_DATA, "4-bit zero point out of [0, 15]");
     return MQ_OK;
 }
 

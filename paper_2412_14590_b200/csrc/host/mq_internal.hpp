@@ -29,6 +29,10 @@ inline int64_t row_stride(int bits, int64_t cols) { return bits == 4 ? (cols + 1
 void pack_nibbles_raw(const uint8_t* v, int64_t n, uint8_t* out);
 int raw_code(const uint8_t* payload, int bits, int64_t cols, int64_t r, int64_t c);
 mq_status validate_desc(const mq_layer_desc* d);
+mq_status validate_maps(const mq_layer_desc* d);
+mq_status check_scheme(const mq_scheme* s);
+mq_status partition_maps(int64_t N, const int32_t* promoted, int64_t np, std::vector<int32_t>& map8,
+                         std::vector<int32_t>& map4);
 float round_scale_f16(float s);
 
 // proj/include/mixquant/rng.hpp:16-82 (SplitMix64 seeding, xoshiro256++,

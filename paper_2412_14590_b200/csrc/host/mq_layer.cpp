@@ -378,11 +378,15 @@ mq_status ensure_internal_ws(mq_layer_s* L, size_t bytes, cudaStream_t stream, v
 
 }  // namespace
 
-extern "C" {
-
-mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int device, mq_layer_t* out) {
+namespace {
+// Layer creation shared by the host packer (mq_layer_create: host reference
+// layouts) and the device packer (mq_layer_create_device: reference layouts
+// already in device memory, packed by wq_engine_kernel). Index maps are host
+// arrays in both cases.
+mq_status create_layer(const mq_layer_desc* d, const mq_layer_opts* opts, int device, bool dev_src,
+                       cudaStream_t stream, mq_layer_t* out) {
     if (!out) return fail(MQ_USAGE, "out handle is null");
-    if (mq_status st = validate_desc(d)) return st;
+    if (mq_status st = dev_src ? validate_maps(d) : validate_desc(d)) return st;
     if (d->group_size != kGroupK)
         return fail(MQ_USAGE, "group size " + std::to_string(d->group_size) +
                                   " not supported by the sm_100a engine (tcgen05 tiles use group 128, the reference default)");
@@ -397,6 +401,21 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
     if (major != 10) return fail(MQ_CUDA, "the engine is built for sm_100a (B200); device is sm_" + std::to_string(major) + "x");
     CU_TRY(cudaSetDevice(device));
+    const int64_t G = num_groups(d->in_features, d->group_size);
+    if (dev_src) {  // validate_quantized's metadata checks (quant.cpp:81-101), on device
+        int32_t* flags = nullptr;
+        CU_TRY(cudaMalloc(&flags, 8));
+        int32_t h[2] = {0, 0};
+        cudaError_t e = cudaMemsetAsync(flags, 0, 8, stream);
+        if (e == cudaSuccess)
+            e = launch_meta_check(d->scales8, d->n8 * G, d->scales4, d->n4 * G, d->zero_points4, flags, stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, flags, 8, cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        cudaFree(flags);
+        if (e != cudaSuccess) return cuda_fail(e, "layer metadata check");
+        if (h[0]) return fail(MQ_DATA, "quantized tensor has a non-positive scale");
+        if (h[1]) return fail(MQ_DATA, "4-bit zero point out of [0, 15]");
+    }
 
     auto* L = new mq_layer_s;
     L->device = device;
@@ -404,11 +423,11 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     L->N = d->out_features;
     L->K = d->in_features;
     L->group = d->group_size;
-    L->G = static_cast<int>(num_groups(L->K, L->group));
+    L->G = static_cast<int>(G);
     L->rank = o.rank;
     L->world = o.world;
     L->w8_mode = o.w8_mode;
-    const int64_t K = L->K, G = L->G;
+    const int64_t K = L->K;
 
     // Shard: rank r owns rows [r*n/W, (r+1)*n/W) of each sub-problem.
     auto lo = [&](int64_t n, int r) { return n * r / o.world; };
@@ -436,14 +455,12 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
         L->shard_cols = L->N;
     }
 
-    // ---- pack (host), then upload once
+    // ---- tiles and the scatter column of every tile row
     const int64_t T = L->tiles8 + L->tiles4;
     L->bytes_wq = (L->tiles8 * kBlock8Bytes + L->tiles4 * kBlock4Bytes) * G;
-    std::vector<uint8_t> wq(size_t(std::max<int64_t>(L->bytes_wq, 1)), 0);
     std::vector<int32_t> colmap(size_t(std::max<int64_t>(T * kTileRows, 1)), -1);
     L->tiles.resize(size_t(T));
     int64_t coff = 0;
-    const int64_t stride4 = row_stride(4, K);
     for (int64_t t = 0; t < T; ++t) {
         const bool is8 = t < L->tiles8;
         const int64_t first = is8 ? t * kTileRows : (t - L->tiles8) * kTileRows;  // local sub row
@@ -461,36 +478,6 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
             colmap[t * kTileRows + r] = o.world > 1 ? static_cast<int32_t>(lcol)
                                                     : (is8 ? d->index_map8[srow] : d->index_map4[srow]);
         }
-        for (int64_t g = 0; g < G; ++g) {
-            const int64_t k0 = g * kGroupK;
-            uint8_t* cb = wq.data() + coff + g * (is8 ? kBlock8Bytes : kBlock4Bytes);
-            uint8_t* mb = cb + (is8 ? kCodes8Bytes : kCodes4Bytes);  // scales | zero points
-            for (int r = 0; r < rows; ++r) {
-                const int64_t srow = (is8 ? a8 : a4) + first + r;
-                float sc;
-                if (is8) {
-                    const uint8_t* src = d->payload8 + srow * K;
-                    for (int k = 0; k < kGroupK && k0 + k < K; ++k) cb[sw128_offset(r, k)] = src[k0 + k];
-                    sc = d->scales8[srow * G + g];
-                } else {
-                    const uint8_t* src = d->payload4 + srow * stride4;
-                    for (int ch = 0; ch < 8; ++ch) {
-                        uint8_t e[16];
-                        for (int j = 0; j < 16; ++j) {
-                            const int64_t k = k0 + ch * 16 + j;
-                            e[j] = k < K ? ((k & 1) ? (src[k / 2] >> 4) : (src[k / 2] & 0x0F)) : 0;
-                        }
-                        uint32_t w0, w1;
-                        pack_chunk4(e, &w0, &w1);
-                        std::memcpy(cb + sub4_chunk_offset(r, ch), &w0, 4);
-                        std::memcpy(cb + sub4_chunk_offset(r, ch) + 4, &w1, 4);
-                    }
-                    sc = d->scales4[srow * G + g];
-                    mb[512 + r] = d->zero_points4[srow * G + g];
-                }
-                std::memcpy(mb + 4 * r, &sc, 4);
-            }
-        }
         coff += (is8 ? kBlock8Bytes : kBlock4Bytes) * G;
         L->stream_bytes += int64_t(is8 ? kBlock8Bytes : kBlock4Bytes) * G;
     }
@@ -500,7 +487,53 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
         if (e != cudaSuccess) return e;
         return n ? cudaMemcpy(*dst, src, n, cudaMemcpyHostToDevice) : cudaSuccess;
     };
-    cudaError_t e = upload(reinterpret_cast<void**>(&L->d_wq), wq.data(), size_t(L->bytes_wq));
+    cudaError_t e = cudaSuccess;
+    if (dev_src) {  // pack on the GPU from the device reference layouts (weight_quant.cu)
+        e = cudaMalloc(reinterpret_cast<void**>(&L->d_wq), std::max<size_t>(size_t(L->bytes_wq), 16));
+        if (e == cudaSuccess)
+            e = launch_engine_pack(static_cast<int32_t>(L->tiles8), static_cast<int32_t>(L->tiles4), L->n8, L->n4, a8,
+                                   a4, L->G, K, d->payload8, d->scales8, d->payload4, d->scales4, d->zero_points4,
+                                   L->d_wq, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    } else {  // pack on the host, upload once
+        std::vector<uint8_t> wq(size_t(std::max<int64_t>(L->bytes_wq, 1)), 0);
+        const int64_t stride4 = row_stride(4, K);
+        for (int64_t t = 0; t < T; ++t) {
+            const TileDesc& td = L->tiles[t];
+            const bool is8 = td.is8 != 0;
+            for (int64_t g = 0; g < G; ++g) {
+                const int64_t k0 = g * kGroupK;
+                uint8_t* cb = wq.data() + td.codes_off + g * (is8 ? kBlock8Bytes : kBlock4Bytes);
+                uint8_t* mb = cb + (is8 ? kCodes8Bytes : kCodes4Bytes);  // scales | zero points
+                for (int r = 0; r < td.rows; ++r) {
+                    const int64_t srow = (is8 ? a8 : a4) + td.first + r;
+                    float sc;
+                    if (is8) {
+                        const uint8_t* src = d->payload8 + srow * K;
+                        for (int k = 0; k < kGroupK && k0 + k < K; ++k) cb[sw128_offset(r, k)] = src[k0 + k];
+                        sc = d->scales8[srow * G + g];
+                    } else {
+                        const uint8_t* src = d->payload4 + srow * stride4;
+                        for (int ch = 0; ch < 8; ++ch) {
+                            uint8_t ev[16];
+                            for (int j = 0; j < 16; ++j) {
+                                const int64_t k = k0 + ch * 16 + j;
+                                ev[j] = k < K ? ((k & 1) ? (src[k / 2] >> 4) : (src[k / 2] & 0x0F)) : 0;
+                            }
+                            uint32_t w0, w1;
+                            pack_chunk4(ev, &w0, &w1);
+                            std::memcpy(cb + sub4_chunk_offset(r, ch), &w0, 4);
+                            std::memcpy(cb + sub4_chunk_offset(r, ch) + 4, &w1, 4);
+                        }
+                        sc = d->scales4[srow * G + g];
+                        mb[512 + r] = d->zero_points4[srow * G + g];
+                    }
+                    std::memcpy(mb + 4 * r, &sc, 4);
+                }
+            }
+        }
+        e = upload(reinterpret_cast<void**>(&L->d_wq), wq.data(), size_t(L->bytes_wq));
+    }
     if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_colmap), colmap.data(), colmap.size() * 4);
     if (e != cudaSuccess) {
         mq_layer_destroy(L);
@@ -509,7 +542,147 @@ mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int
     *out = L;
     return MQ_OK;
 }
+}  // namespace
 
+extern "C" {
+
+mq_status mq_layer_create(const mq_layer_desc* d, const mq_layer_opts* opts, int device, mq_layer_t* out) {
+    return create_layer(d, opts, device, false, nullptr, out);
+}
+
+mq_status mq_layer_create_device(const mq_layer_desc* d, const mq_layer_opts* opts, int device, void* stream,
+                                 mq_layer_t* out) {
+    return create_layer(d, opts, device, true, static_cast<cudaStream_t>(stream), out);
+}
+
+mq_status mq_layer_export_packed(mq_layer_t L, void* wq_host, size_t bytes, int32_t* colmap_host) {
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
+    if (bytes != size_t(L->bytes_wq)) return fail(MQ_USAGE, "export buffer must be mq_layer_info.device_bytes bytes");
+    cudaError_t e = cudaMemcpy(wq_host, L->d_wq, bytes, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && colmap_host)
+        e = cudaMemcpy(colmap_host, L->d_colmap, size_t(L->tiles8 + L->tiles4) * kTileRows * 4,
+                       cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "export packed layer");
+    return MQ_OK;
+}
+
+// ------------------------------------------------- GPU partition_and_quantize
+struct mq_device_qlayer_s {
+    int device = 0;
+    int64_t N = 0, K = 0;
+    int group = 128;
+    mq_scheme large{}, small{};
+    std::vector<int32_t> map8, map4;
+    uint8_t *p8 = nullptr, *p4 = nullptr, *z8 = nullptr, *z4 = nullptr;
+    float *s8 = nullptr, *s4 = nullptr;
+};
+
+void mq_device_qlayer_destroy(mq_device_qlayer_t h) {
+    if (!h) return;
+    for (void* p : {static_cast<void*>(h->p8), static_cast<void*>(h->p4), static_cast<void*>(h->z8),
+                    static_cast<void*>(h->z4), static_cast<void*>(h->s8), static_cast<void*>(h->s4)})
+        if (p) cudaFree(p);
+    delete h;
+}
+
+mq_status mq_partition_and_quantize_device(const double* W, int64_t N, int64_t K, const int32_t* promoted, int64_t np,
+                                           const mq_scheme* large, const mq_scheme* small, int device, void* stream,
+                                           mq_device_qlayer_t* out) {
+    if (!out) return fail(MQ_USAGE, "out handle is null");
+    if (!W && N * K > 0) return fail(MQ_USAGE, "weight matrix is null");
+    if (mq_status st = check_scheme(large)) return st;
+    if (mq_status st = check_scheme(small)) return st;
+    if (large->group_size != small->group_size)
+        return fail(MQ_DATA, "mixed layer: sub-problems must share group boundaries");
+    for (const mq_scheme* sc : {large, small})
+        if (sc->bit_width == 4 && sc->symmetric)
+            return fail(MQ_USAGE, "quantize_tensor: 4-bit symmetric tensors are not supported");
+    CU_TRY(cudaSetDevice(device));
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto* h = new mq_device_qlayer_s;
+    h->device = device;
+    h->N = N;
+    h->K = K;
+    h->group = large->group_size;
+    h->large = *large;
+    h->small = *small;
+    if (mq_status st = partition_maps(N, promoted, np, h->map8, h->map4)) {
+        delete h;
+        return st;
+    }
+    const int64_t G = num_groups(K, h->group);
+    int32_t* d_err = nullptr;
+    int32_t* d_map = nullptr;
+    uint8_t* d_codes = nullptr;
+    int32_t herr[2] = {INT32_MAX, INT32_MAX};
+    const int64_t n8 = int64_t(h->map8.size()), n4 = int64_t(h->map4.size());
+    cudaError_t e = cudaMalloc(&d_err, 8);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_err, herr, 8, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMalloc(&d_map, size_t(std::max<int64_t>(N, 1)) * 4);
+    // sub8 (large-bit) then sub4 (small-bit): gather + quantize in one pass per sub-problem
+    for (int w = 0; w < 2 && e == cudaSuccess; ++w) {
+        const mq_scheme* sc = w ? small : large;
+        const std::vector<int32_t>& map = w ? h->map4 : h->map8;
+        const int64_t rows = w ? n4 : n8;
+        uint8_t*& pay = w ? h->p4 : h->p8;
+        float*& scl = w ? h->s4 : h->s8;
+        uint8_t*& zp = w ? h->z4 : h->z8;
+        const int64_t stride = row_stride(sc->bit_width, K);
+        e = cudaMalloc(&pay, size_t(std::max<int64_t>(rows * stride, 16)));
+        if (e == cudaSuccess) e = cudaMalloc(&scl, size_t(std::max<int64_t>(rows * G, 4)) * 4);
+        if (e == cudaSuccess && !sc->symmetric) e = cudaMalloc(&zp, size_t(std::max<int64_t>(rows * G, 16)));
+        if (e == cudaSuccess && rows > 0)
+            e = cudaMemcpyAsync(d_map, map.data(), size_t(rows) * 4, cudaMemcpyHostToDevice, s);
+        uint8_t* codes = pay;
+        if (e == cudaSuccess && sc->bit_width == 4) {  // one byte per code, then the nibble packer
+            if (d_codes) cudaFree(d_codes);
+            d_codes = nullptr;
+            e = cudaMalloc(&d_codes, size_t(std::max<int64_t>(rows * K, 16)));
+            codes = d_codes;
+        }
+        if (e == cudaSuccess)
+            e = launch_weight_quant(W, K, d_map, rows, h->group, sc->bit_width, sc->symmetric, sc->scale_f16_storage,
+                                    codes, scl, zp, d_err + w, s);
+        if (e == cudaSuccess && sc->bit_width == 4) e = launch_pack_nibbles(codes, rows, K, pay, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // d_map / d_codes are reused
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(herr, d_err, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d_err);
+    cudaFree(d_map);
+    if (d_codes) cudaFree(d_codes);
+    if (e != cudaSuccess) {
+        mq_device_qlayer_destroy(h);
+        return cuda_fail(e, "device partition_and_quantize");
+    }
+    for (int w = 0; w < 2; ++w)
+        if (herr[w] != INT32_MAX) {  // the reference throws at the first failing group (sub8 first)
+            const int64_t r = herr[w] / G, g = herr[w] % G;
+            mq_device_qlayer_destroy(h);
+            return fail(MQ_DATA, "row " + std::to_string(r) + ", group " + std::to_string(g) +
+                                     ": quantize: non-finite input value");
+        }
+    *out = h;
+    return MQ_OK;
+}
+
+mq_status mq_device_qlayer_desc(mq_device_qlayer_t h, mq_layer_desc* d) {
+    if (!h || !d) return fail(MQ_USAGE, "null device layer");
+    if (h->large.bit_width != 8 || !h->large.symmetric || h->small.bit_width != 4 || h->small.symmetric)
+        return fail(MQ_USAGE, "engine requires 8-bit symmetric / 4-bit asymmetric sub-problems");
+    d->out_features = h->N;
+    d->in_features = h->K;
+    d->group_size = h->group;
+    d->n8 = static_cast<int64_t>(h->map8.size());
+    d->n4 = static_cast<int64_t>(h->map4.size());
+    d->index_map8 = h->map8.data();
+    d->index_map4 = h->map4.data();
+    d->payload8 = h->p8;
+    d->scales8 = h->s8;
+    d->payload4 = h->p4;
+    d->scales4 = h->s4;
+    d->zero_points4 = h->z4;
+    return MQ_OK;
+}
 
 void mq_layer_destroy(mq_layer_t L) {
     if (!L) return;

@@ -159,6 +159,17 @@ cudaError_t launch_repack_eal(const int8_t* codes, int64_t ldc, const float* sca
 cudaError_t launch_permute(const void* gathered, const int32_t* colmap, int world, int64_t shard_cols,
                            int64_t M, int64_t N, void* Y, int dtype, cudaStream_t stream);
 
+// Offline weight quantization / prepack on the GPU (weight_quant.cu).
+cudaError_t launch_weight_quant(const double* W, int64_t K, const int32_t* map, int64_t rows, int group, int bits,
+                                int sym, int f16, uint8_t* codes, float* scales, uint8_t* zp, int32_t* err,
+                                cudaStream_t stream);
+cudaError_t launch_pack_nibbles(const uint8_t* codes, int64_t rows, int64_t K, uint8_t* payload, cudaStream_t stream);
+cudaError_t launch_engine_pack(int32_t T8, int32_t T4, int64_t n8, int64_t n4, int64_t a8, int64_t a4, int32_t G,
+                               int64_t K, const uint8_t* payload8, const float* scales8, const uint8_t* payload4,
+                               const float* scales4, const uint8_t* zp4, uint8_t* wq, cudaStream_t stream);
+cudaError_t launch_meta_check(const float* s8, int64_t n8, const float* s4, int64_t n4, const uint8_t* zp4,
+                              int32_t* flags, cudaStream_t stream);
+
 // Tile descriptor of tile t (sub8 tiles first), identical to the host packer.
 struct TileInfo {
     int64_t off;     // byte offset of the tile's group-0 block

@@ -183,6 +183,84 @@ def partition_and_quantize(weight: np.ndarray, promoted, largebit: QuantScheme =
         lib().mq_host_layer_destroy(h)
 
 
+class DeviceQuantizedLayer:
+    """partition_and_quantize on the GPU (mq_partition_and_quantize_device):
+    the reference layouts stay in device memory (owned here); index maps on
+    the host. `to_host()` copies them into a MixedLinearLayer (e.g. for
+    save_quantized_model); `DeviceLayer.from_device(...)` packs the engine
+    layout on the GPU."""
+
+    def __init__(self, handle, device: int, largebit: QuantScheme, smallbit: QuantScheme, name: str = ""):
+        self.h = handle
+        self.device = device
+        self.largebit, self.smallbit, self.name = largebit, smallbit, name
+        self.d = capi.mq_layer_desc()
+        check(lib().mq_device_qlayer_desc(handle, C.byref(self.d)))
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                lib().mq_device_qlayer_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def to_host(self) -> MixedLinearLayer:
+        d = self.d
+        K = d.in_features
+        G = 0 if K == 0 else (K + d.group_size - 1) // d.group_size
+
+        def dev(ptr, n, dt):
+            if n == 0:
+                return np.zeros((0,), dt)
+            nbytes = n * np.dtype(dt).itemsize
+            return _device_view(ptr, nbytes, self.device).cpu().numpy().view(dt).copy()
+
+        def host(ptr, n, dt):
+            if n == 0:
+                return np.zeros((0,), dt)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(np.ctypeslib.as_ctypes_type(dt))), (n,)).copy()
+
+        n8, n4, s4 = d.n8, d.n4, (K + 1) // 2
+        sub8 = QuantizedTensor(self.largebit, n8, K, dev(d.payload8, n8 * K, np.uint8).reshape(n8, K),
+                               dev(d.scales8, n8 * G, np.float32).reshape(n8, G), None)
+        sub4 = QuantizedTensor(self.smallbit, n4, K, dev(d.payload4, n4 * s4, np.uint8).reshape(n4, s4),
+                               dev(d.scales4, n4 * G, np.float32).reshape(n4, G),
+                               dev(d.zero_points4, n4 * G, np.uint8).reshape(n4, G))
+        return MixedLinearLayer(self.name, d.out_features, K, sub8, sub4, host(d.index_map8, n8, np.int32),
+                                host(d.index_map4, n4, np.int32))
+
+
+def _device_view(ptr, nbytes: int, device: int):
+    """A uint8 CUDA tensor view of `nbytes` at a raw device pointer owned by the
+    library (torch as plumbing: __cuda_array_interface__, no copy, no ownership)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (int(ptr), False), "version": 3,
+                                    "strides": None}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Arr(), device=f"cuda:{device}")
+
+
+def partition_and_quantize_device(weight, promoted, largebit: QuantScheme = LARGEBIT,
+                                  smallbit: QuantScheme = SMALLBIT, name: str = "",
+                                  stream=None) -> DeviceQuantizedLayer:
+    """partition_and_quantize (mixed.cpp:46-81) on the GPU, bit-exact with the
+    host version: weight is a CUDA float64 [N, K] tensor."""
+    import torch
+    if not (isinstance(weight, torch.Tensor) and weight.is_cuda and weight.dtype == torch.float64):
+        raise UsageError("partition_and_quantize_device expects a CUDA float64 weight tensor")
+    W = weight.contiguous()
+    N, K = W.shape
+    prom = np.ascontiguousarray(np.asarray(promoted, np.int32).reshape(-1))
+    h = C.c_void_p()
+    check(lib().mq_partition_and_quantize_device(_p(W), N, K, _p(prom), prom.size, C.byref(largebit.c()),
+                                                 C.byref(smallbit.c()), W.device.index, _stream(stream), C.byref(h)))
+    return DeviceQuantizedLayer(h, W.device.index, largebit, smallbit, name)
+
+
 # ------------------------------------------------------- quantized model I/O
 # "mixquant-quantized-v1" directories (mixed.cpp:208-370): quantized.json plus
 # raw little-endian tensors per sub-problem — <layer>.sub{8,4}.codes.bin u8
@@ -412,6 +490,30 @@ class DeviceLayer:
         self.info = capi.mq_layer_info()
         check(lib().mq_layer_get_info(h, C.byref(self.info)))
         self._ws = {}
+
+    @classmethod
+    def from_device(cls, dq: "DeviceQuantizedLayer", device: int | None = None, w8_mode: int = capi.MQ_W8_REFERENCE,
+                    rank: int = 0, world: int = 1, stream=None) -> "DeviceLayer":
+        """mq_layer_create_device: pack the engine layout on the GPU from a
+        device-quantized layer (no host round trip)."""
+        self = cls.__new__(cls)
+        self.layer = None
+        self.device = dq.device if device is None else device
+        opts = capi.mq_layer_opts(w8_mode, rank, world)
+        h = C.c_void_p()
+        check(lib().mq_layer_create_device(C.byref(dq.d), C.byref(opts), self.device, _stream(stream), C.byref(h)))
+        self.h = h
+        self.info = capi.mq_layer_info()
+        check(lib().mq_layer_get_info(h, C.byref(self.info)))
+        self._ws = {}
+        return self
+
+    def export_packed(self):
+        """(packed engine layout bytes, tile-row column map) copied to host."""
+        wq = np.zeros(self.info.device_bytes, np.uint8)
+        cm = np.zeros((self.info.tiles8 + self.info.tiles4) * 128, np.int32)
+        check(lib().mq_layer_export_packed(self.h, _p(wq), wq.nbytes, _p(cm)))
+        return wq, cm
 
     def __del__(self):
         h = getattr(self, "h", None)
