@@ -145,6 +145,38 @@ def measure_int8_peak(torch):
 
 
 # ------------------------------------------------------------------ ours
+L2_BYTES = 126 << 20
+INT8_SPEC_TOPS = 4500.0  # B200 dense int8 tensor-core spec
+# BASELINE configs[2]: Llama-3.1-70B linear shapes (hidden 8192, FFN 28672), fused like the 8B stack
+SHAPES_70B = [("qkv_proj", 8192 + 1024 + 1024, 8192), ("o_proj", 8192, 8192),
+              ("gate_up_proj", 2 * 28672, 8192), ("down_proj", 8192, 28672)]
+SWEEP_M = (1, 16, 64, 256, 512)
+
+
+def graph_of(torch, fn):
+    """fn() captured into a CUDA graph (after one eager warm-up call)."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g
+
+
+def time_graph_us(torch, g, reps, warmup=3):
+    """Device time of one replay (CUDA events on the replay stream, after warm-up)."""
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e3 / reps
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -162,16 +194,20 @@ def run_ours(args):
     M = args.batch
     hbm_peak, peak_kind = peaks()
 
-    # ---- host: quantize the stack once (reference layouts, bit-exact)
+    # ---- host: quantize the stack once (reference layouts, bit-exact; the
+    # run_bench generator, so the reference arm sees the same weights)
     host = []
     for i, (name, N, K) in enumerate(SHAPES_8B):
         W, A, prom = mq.bench_inputs(1, N, K, PERCENT, 1 + i)
         host.append((name, N, K, mq.partition_and_quantize(W, prom, name=name)))
-    R = 2 if world == 1 else 1  # device replicas rotated between steps (> L2)
-    layers = [[mq.DeviceLayer(L, local, rank=rank, world=world) for (_, _, _, L) in host] for _ in range(R)]
+    stack_bytes = sum(L.sub8.rows * K + L.sub4.rows * K // 2 for (_, _, K, L) in host)
+    # device replicas rotated between steps: >= 3x L2 of weights (L2 hygiene)
+    R = max(3, -(-3 * L2_BYTES // stack_bytes)) if world == 1 else 1
+    reps = [mq.DeviceLayer.replicas(L, R, local, rank=rank, world=world) for (_, _, _, L) in host]
+    layers = [[reps[i][r] for i in range(len(host))] for r in range(R)]
     mode = capi.MQ_FAST if args.mode == "fast" else capi.MQ_EXACT
 
-    def make_io(m, act_group):
+    def make_io(m, act_group, mode=mode):
         g = torch.Generator(device=dev).manual_seed(1234 + m)
         xs = [torch.randn((m, K), generator=g, device=dev, dtype=torch.float32) for (_, _, K, _) in host]
         ys = [torch.empty((m, layers[0][i].out_cols), dtype=torch.float16, device=dev) for i in range(len(host))]
@@ -214,18 +250,10 @@ def run_ours(args):
         return float(ms.item()) / steps
 
     def graphs_for(fn_of_r):
-        out = []
-        for r in range(R):
-            fn_of_r(r)  # eager warm-up: workspaces, attributes
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                fn_of_r(r)
-            out.append(g.replay)
-        return out
+        return [graph_of(torch, lambda r=r: fn_of_r(r)).replay for r in range(R)]
 
-    def bench_batch(m, act_group, steps, warmup, sampler=None):
-        xs, ys, opts = make_io(m, act_group)
+    def bench_batch(m, act_group, steps, warmup, sampler=None, mode=mode):
+        xs, ys, opts = make_io(m, act_group, mode)
         nonlocal gathered, finals
         if world > 1:
             gathered = [torch.empty((world, m, layers[0][i].out_cols), dtype=torch.float16, device=dev)
@@ -236,6 +264,7 @@ def run_ours(args):
                 f()
         else:
             fns = graphs_for(lambda r: step(r, xs, ys, opts, m))
+
         def ramp():  # pre-ramp clocks (not counted as steps)
             t_end = time.time() + 0.3
             while time.time() < t_end:
@@ -265,7 +294,30 @@ def run_ours(args):
     head = bench_batch(M, GROUP, args.steps, args.warmup, sampler)
     ms = head["ms"]
     value = head["ops"] / (ms * 1e-3) / 1e12
-    achieved = head["k2_bytes"] / (head["ms_k2"] * 1e-3) / 1e9  # GB/s over the 7 K2 launches
+    achieved = head["k2_bytes"] / (head["ms_k2"] * 1e-3) / 1e9  # GB/s over the 4 K2 launches
+
+    def fracs(byts, ops, us):
+        t = us * 1e-6
+        return {"k2_hbm_frac": round(byts / t / 1e9 / hbm_peak, 3),
+                "k2_int8_tc_frac": round(ops / t / 1e12 / int8_peak, 3) if int8_peak else None,
+                "k2_int8_spec_frac": round(ops / t / 1e12 / INT8_SPEC_TOPS, 3)}
+
+    # ---- per-layer K2 at the headline batch: each projection alone, rotating
+    # through enough GPU-packed copies of it that its weights exceed 3x L2
+    per_layer = {}
+    if world == 1 and not args.no_sweep:
+        xs, ys, opts = head["xs"], head["ys"], head["opts"]
+        for i, (name, N, K, L) in enumerate(host):
+            lb = L.sub8.rows * K + L.sub4.rows * K // 2
+            n = max(4, -(-3 * L2_BYTES // lb))
+            copies = mq.DeviceLayer.replicas(L, n, local)
+            ws = copies[0].quantize_ws(xs[i], opts)
+            g = graph_of(torch, lambda: [c.forward_ws(M, ws, out=ys[i], opts=opts) for c in copies])
+            us = time_graph_us(torch, g, max(5, args.steps // 2)) / n
+            byts = k2_bytes(M, N, K, L.sub8.rows, L.sub4.rows)
+            per_layer[name] = {"shape": f"{N}x{K}", "k2_us": round(us, 2), "bytes": int(byts),
+                               **fracs(byts, 2.0 * M * N * K, us)}
+            del copies, g
 
     # ---- e2e through the public C-ABI path with host buffers (pinned), N GPUs
     e2e = None
@@ -283,8 +335,6 @@ def run_ours(args):
         yv = list(torch.split(dy_all, ny))
         xv = [v.view(x.shape) for v, x in zip(xv, xs)]
         yv = [v.view(y.shape) for v, y in zip(yv, ys)]
-        hx = [hx_all]
-        hy = [hy_all]
 
         # per-layer copies on the two copy engines, overlapped with the other
         # layers' kernels (a pipelined serving step): layer i's forward waits
@@ -328,25 +378,38 @@ def run_ours(args):
             torch.cuda.synchronize()
         ems = timed(efns, args.steps, args.warmup)
         e2e = {"value": head["ops"] / (ems * 1e-3) / 1e12, "unit": "TOPS",
-               "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in hx)),
-               "d2h_bytes_per_step": int(sum(y.numel() * 2 for y in hy)), "ms_per_step": ems}
+               "h2d_bytes_per_step": int(hx_all.numel() * 4),
+               "d2h_bytes_per_step": int(hy_all.numel() * 2), "ms_per_step": ems}
 
-    # ---- batch sweep (BASELINE metric is "vs batch 1-512")
+    # ---- batch sweep (BASELINE metric is "vs batch 1-512"), FAST mode, plus
+    # per-token activations and the bit-exact parity mode at 16 and 512
     sweep = {}
     if world == 1 and not args.no_sweep:
-        for m in (1, 16, 64, 256, 512):
-            for ag_name, ag in (("group", GROUP), ("token", 1 << 30)):
-                if ag_name == "token" and m not in (16, 512):
+        for m in SWEEP_M:
+            for var, ag, md in (("", GROUP, capi.MQ_FAST), ("_per_token", 1 << 30, capi.MQ_FAST),
+                                ("_exact", GROUP, capi.MQ_EXACT)):
+                if var and m not in (16, 512):
                     continue
-                r = bench_batch(m, ag, max(10, args.steps // 4), 3)
-                key = f"M{m}" + ("" if ag_name == "group" else "_per_token")
-                t2 = r["ms_k2"] * 1e-3
-                sweep[key] = {"tops": round(r["ops"] / (r["ms"] * 1e-3) / 1e12, 2),
-                              "us_per_stack": round(r["ms"] * 1e3, 2),
-                              "k2_us_per_stack": round(r["ms_k2"] * 1e3, 2),
-                              "k2_hbm_frac": round(r["k2_bytes"] / t2 / 1e9 / hbm_peak, 3),
-                              "k2_int8_tc_frac": (round(r["ops"] / t2 / 1e12 / int8_peak, 3) if int8_peak else None)}
+                r = bench_batch(m, ag, max(10, args.steps // 4), 3, mode=md)
+                sweep[f"M{m}{var}"] = {"tops": round(r["ops"] / (r["ms"] * 1e-3) / 1e12, 2),
+                                       "us_per_stack": round(r["ms"] * 1e3, 2),
+                                       "k2_us_per_stack": round(r["ms_k2"] * 1e3, 2),
+                                       **fracs(r["k2_bytes"], r["ops"], r["ms_k2"] * 1e3)}
                 del r
+
+    # ---- C1 (BASELINE configs[0]): the single K=N=4096 linear at batch 16 on
+    # the reference's own run_bench inputs (seed 1): device time, roofline,
+    # the exact-mode checksum against the reference's, and the reference's
+    # own CPU time for the same call on this host
+    c1 = None
+    if world == 1 and not args.no_sweep:
+        c1 = c1_line(torch, mq, capi, local, hbm_peak, int8_peak, fracs, args)
+
+    # ---- C3 (BASELINE configs[2]): the 70B stack, weights quantized and
+    # packed on the GPU (mq_partition_and_quantize_device)
+    c3 = None
+    if world == 1 and not args.no_sweep and not args.no_70b:
+        c3 = sweep_70b(torch, mq, capi, local, fracs, args)
 
     # ---- C5 (BASELINE configs[4]): the same stack with the 8-bit fraction swept
     # 0-20%, at batch 1 and 512 (device-resident, K1 + K2, CUDA graph)
@@ -356,17 +419,12 @@ def run_ours(args):
             stack = []
             for i, (name, N, K) in enumerate(SHAPES_8B):
                 W, _, prom = mq.bench_inputs(1, N, K, pct, 1 + i)
-                stack.append(mq.DeviceLayer(mq.partition_and_quantize(W, prom, name=name), local))
+                stack.append(mq.DeviceLayer.replicas(mq.partition_and_quantize(W, prom, name=name), R, local))
             for m in (1, 512):
                 xs_p, ys_p, opts_p = make_io(m, GROUP)
-
-                def fwd(r, xs_p=xs_p, ys_p=ys_p, opts_p=opts_p):
-                    for i in range(len(stack)):
-                        stack[i].forward(xs_p[i], out=ys_p[i], opts=opts_p)
-                g = graphs_for(fwd)[0]
-                for _ in range(3):
-                    g()
-                ms_p = timed([g], max(10, args.steps // 4), 3)
+                gs = [graph_of(torch, lambda r=r: [stack[i][r].forward(xs_p[i], out=ys_p[i], opts=opts_p)
+                                                   for i in range(len(stack))]).replay for r in range(R)]
+                ms_p = timed(gs, max(10, args.steps // 4), 3)
                 ops_p = sum(2.0 * m * N * K for (_, N, K, _) in host)
                 c5[f"p{int(round(pct * 100))}_M{m}"] = {"tops": round(ops_p / (ms_p * 1e-3) / 1e12, 2),
                                                         "us_per_stack": round(ms_p * 1e3, 2)}
@@ -393,21 +451,103 @@ def run_ours(args):
                                    f"A8 group-wise (reference semantics); mode {args.mode}; fp16 out",
                        "batch": M, "group": GROUP, "percent_8bit": PERCENT,
                        "parallelism": f"column-shard x{world}" if world > 1 else "single",
-                       "l2": "2 device replicas of the stack (~256 MB) alternate between steps (> 126 MB L2)",
+                       "l2": f"{R} device replicas of the stack ({R * stack_bytes / 2**20:.0f} MB of weights, "
+                             f">= 3x the 126 MB L2) rotate between steps",
                        "cuda_graph": world == 1},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": k2_traffic(M),
                          "kernel": f"mixed_gemm_tc_kernel ({len(SHAPES_8B)} launches/step; bytes and time summed)",
                          "peak_kind": peak_kind,
-                         "k2_bytes_per_step": int(head["k2_bytes"]), "k2_ms_per_step": round(head["ms_k2"], 5)},
+                         "k2_bytes_per_step": int(head["k2_bytes"]), "k2_ms_per_step": round(head["ms_k2"], 5),
+                         "per_layer": per_layer},
             "int8_peak_tops_measured": round(int8_peak, 1) if int8_peak else None,
+            "int8_peak_tops_spec": INT8_SPEC_TOPS,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps * 2 * len(SHAPES_8B), "clocks": clocks,
             "sweep": sweep,
+            "c1": c1,
+            "c3_70b": c3,
             "c5_percent_8bit_sweep": c5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def c1_line(torch, mq, capi, local, hbm_peak, int8_peak, fracs, args):
+    """BASELINE configs[0] on its own: K = N = 4096, batch 16, p = 0.10, the
+    reference run_bench generator with seed 1 (its golden checksum is
+    5bb508ecbf3b895f)."""
+    import oracle_py as O
+
+    m, n, k = 16, 4096, 4096
+    W, A, prom = mq.bench_inputs(m, n, k, PERCENT, 1)
+    L = mq.partition_and_quantize(W, prom)
+    nrep = max(4, -(-3 * L2_BYTES // (L.sub8.rows * k + L.sub4.rows * k // 2)))
+    copies = mq.DeviceLayer.replicas(L, nrep, local)
+    dA = torch.from_numpy(A).to(f"cuda:{local}")
+    out = {"shape": f"{n}x{k}", "batch": m, "replicas": nrep}
+    ref_sum = None
+    for name, md in (("fast", capi.MQ_FAST), ("exact", capi.MQ_EXACT)):
+        opts = mq.exec_opts(md, GROUP)
+        y = torch.empty((m, n), dtype=torch.float32, device=dA.device)
+        g = graph_of(torch, lambda: [c.forward(dA, out=y, opts=opts) for c in copies])
+        us = time_graph_us(torch, g, max(5, args.steps // 2)) / nrep
+        ws = copies[0].quantize_ws(dA, opts)
+        g2 = graph_of(torch, lambda: [c.forward_ws(m, ws, out=y, opts=opts) for c in copies])
+        k2us = time_graph_us(torch, g2, max(5, args.steps // 2)) / nrep
+        byts = k2_bytes(m, n, k, L.sub8.rows, L.sub4.rows, out_bytes=4)
+        out[name] = {"us": round(us, 2), "k2_us": round(k2us, 2), **fracs(byts, 2.0 * m * n * k, k2us)}
+        if name == "exact":
+            copies[0].forward(dA, out=y, opts=opts)
+            ref_sum = mq.fnv1a_hex(y.cpu().numpy())
+            out["exact"]["checksum"] = ref_sum
+    if O.ref_available() and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        r = O.ref_run_bench(m, n, k, PERCENT, workers=cores, repeats=5)
+        out["cpu_baseline"] = {"ms_per_call": round(r["wall_ms"] / 5, 2), "gops": round(r["gops"], 3),
+                               "cores": cores, "kind": "reference",
+                               "sample": "reference run_bench(16, 4096, 4096, 0.10), 5 repeats, workers = cores",
+                               "checksum": r["checksum"]}
+        out["exact"]["checksum_equals_reference"] = r["checksum"] == ref_sum
+    return out
+
+
+def sweep_70b(torch, mq, capi, local, fracs, args):
+    """BASELINE configs[2]: Llama-3.1-70B linear shapes x batch sweep on one
+    B200. Weights are N(0, 1) f64 drawn on the device, 10% promoted at random,
+    quantized and packed on the GPU (bit-exact with the host path, see
+    tests/test_gpu_weight_quant.py). One copy of the stack (~0.5 GB > 3x L2)."""
+    dv = f"cuda:{local}"
+    gen = torch.Generator(device=dv).manual_seed(70)
+    rng = np.random.default_rng(70)
+    layers, qsec = [], {}
+    for name, N, K in SHAPES_70B:
+        t0 = time.time()
+        W = torch.randn((N, K), generator=gen, dtype=torch.float64, device=dv)
+        prom = rng.permutation(N)[: int(round(PERCENT * N))].astype(np.int32)
+        dq = mq.partition_and_quantize_device(W, prom, name=name)
+        del W
+        layers.append((name, N, K, mq.DeviceLayer.from_device(dq)))
+        del dq
+        torch.cuda.synchronize()
+        qsec[name] = round(time.time() - t0, 2)
+    out = {"shapes": {n: f"{N}x{K}" for (n, N, K, _) in layers}, "gpu_quantize_pack_s": qsec}
+    for m in SWEEP_M:
+        xs = [torch.randn((m, K), device=dv) for (_, _, K, _) in layers]
+        ys = [torch.empty((m, N), dtype=torch.float16, device=dv) for (_, N, _, _) in layers]
+        opts = mq.exec_opts(capi.MQ_FAST, GROUP)
+        g = graph_of(torch, lambda: [d.forward(xs[i], out=ys[i], opts=opts) for i, (_, _, _, d) in enumerate(layers)])
+        us = time_graph_us(torch, g, max(5, args.steps // 4))
+        wss = [d.quantize_ws(xs[i], opts) for i, (_, _, _, d) in enumerate(layers)]
+        g2 = graph_of(torch, lambda: [d.forward_ws(m, wss[i], out=ys[i], opts=opts)
+                                      for i, (_, _, _, d) in enumerate(layers)])
+        k2us = time_graph_us(torch, g2, max(5, args.steps // 4))
+        ops = sum(2.0 * m * N * K for (_, N, K, _) in layers)
+        byts = sum(k2_bytes(m, N, K, d.info.n8, d.info.n4) for (_, N, K, d) in layers)
+        out[f"M{m}"] = {"tops": round(ops / (us * 1e-6) / 1e12, 2), "us_per_stack": round(us, 2),
+                        "k2_us_per_stack": round(k2us, 2), **fracs(byts, ops, k2us)}
+        del g, g2, wss
+    return out
 
 
 # ----------------------------------------------------------- reference
@@ -500,6 +640,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-70b", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -508,6 +508,32 @@ class DeviceLayer:
         self._ws = {}
         return self
 
+    @classmethod
+    def replicas(cls, layer: MixedLinearLayer, n: int, device: int = 0, w8_mode: int = capi.MQ_W8_REFERENCE,
+                 rank: int = 0, world: int = 1) -> list:
+        """n independent device copies of one layer: the reference layouts are
+        uploaded once and each copy is packed on the GPU (mq_layer_create_device)
+        — benchmarks rotate copies so the weights stream from HBM, not L2."""
+        import torch
+        dv = f"cuda:{device}"
+        keep = [torch.from_numpy(np.ascontiguousarray(a)).to(dv) for a in
+                (layer.sub8.payload, layer.sub8.scales, layer.sub4.payload, layer.sub4.scales,
+                 layer.sub4.zero_points if layer.sub4.zero_points is not None else np.zeros((1,), np.uint8))]
+        d = layer.desc()  # host maps (kept alive by `layer`)
+        (d.payload8, d.scales8, d.payload4, d.scales4, d.zero_points4) = [t.data_ptr() for t in keep]
+        out = []
+        for _ in range(n):
+            self = cls.__new__(cls)
+            self.layer, self.device, self._ws = layer, device, {}
+            h = C.c_void_p()
+            check(lib().mq_layer_create_device(C.byref(d), C.byref(capi.mq_layer_opts(w8_mode, rank, world)), device,
+                                               None, C.byref(h)))
+            self.h = h
+            self.info = capi.mq_layer_info()
+            check(lib().mq_layer_get_info(h, C.byref(self.info)))
+            out.append(self)
+        return out
+
     def export_packed(self):
         """(packed engine layout bytes, tile-row column map) copied to host."""
         wq = np.zeros(self.info.device_bytes, np.uint8)
