@@ -320,6 +320,53 @@ mq_status mq_permute_gathered(const void* gathered, const int32_t* colmap_dev, i
                               int64_t shard_cols, int64_t M, int64_t out_features, void* Y,
                               mq_dtype dtype, void* stream);
 
+/* ===================================================================== */
+/* Multi-GPU: output-feature column sharding (no reference     */
+/* counterpart — the reference is single-process). Layers are created with */
+/* mq_layer_opts {rank, world}: rank r owns sub8 rows [r*n8/W, (r+1)*n8/W)  */
+/* and the same slice of sub4 rows; activations are replicated.            */
+/* ===================================================================== */
+
+/* NCCL communicators. The library binds NCCL at run time (dlopen): the NCCL
+ * already loaded in the process is used first (e.g. PyTorch's, so a
+ * ProcessGroupNCCL communicator can be passed as `comm`), else libnccl.so.2.
+ * id: NCCL_UNIQUE_ID_BYTES (128) bytes, created on one rank and shared. */
+mq_status mq_nccl_unique_id(uint8_t* id);
+mq_status mq_nccl_comm_init(const uint8_t* id, int32_t world, int32_t rank, int device, void** comm);
+mq_status mq_nccl_comm_destroy(void* comm);
+
+/* Gathered forward of one shard (north_star: NCCL all-gather over NVLink for
+ * the gathered output only): K1 + K2 into this rank's [M, shard_cols] block in
+ * gather order, ncclAllGather of the blocks on `comm` (an ncclComm_t whose rank
+ * and size must match the layer's), then the permute to original column order
+ * into Y [M, out_features]. Stream-ordered on `stream`; the workspace
+ * (mq_mixed_linear_allgather_workspace_bytes) holds the forward scratch, the
+ * local block and the gathered blocks. Equal, bit for bit, to the unsharded
+ * layer's mq_mixed_linear under the same options. */
+size_t mq_mixed_linear_allgather_workspace_bytes(mq_layer_t layer, int64_t M, const mq_exec_opts* opts,
+                                                 mq_dtype out_dtype);
+mq_status mq_mixed_linear_allgather(mq_layer_t layer, const void* A, mq_dtype a_dtype, int64_t M, void* Y,
+                                    mq_dtype out_dtype, const mq_exec_opts* opts, void* workspace,
+                                    int32_t* err, void* comm, void* stream);
+
+/* Fused gather: the K2 epilogue scatters every output
+ * element of this shard straight into ALL ranks' full outputs at the original
+ * column — y_peers[i] is rank i's Y [M, out_features], peer-mapped into this
+ * process (cudaIpcOpenMemHandle / NVLink UVA, or an NCCL window's LSA
+ * pointer); y_peers[0] may be any rank's. No gather buffer, no permute: once
+ * every rank's launch is complete (mq_peer_barrier) each Y is whole. n_peers
+ * <= 8 (one NVLink domain). Workspace as mq_mixed_linear. */
+mq_status mq_mixed_linear_peers(mq_layer_t layer, const void* A, mq_dtype a_dtype, int64_t M,
+                                void* const* y_peers, int32_t n_peers, mq_dtype out_dtype,
+                                const mq_exec_opts* opts, void* workspace, int32_t* err, void* stream);
+
+/* Cross-rank completion barrier for the fused gather: flags[i] is rank i's
+ * uint32 flag array [world] (peer-mapped, zero-initialised); rank `rank`
+ * release-stores `epoch` into flags[i][rank] for every i, then waits until its
+ * own flags[rank][0..world) all reached `epoch` (system-scope acquire). Use a
+ * new epoch per call. One tiny kernel on `stream`. */
+mq_status mq_peer_barrier(uint32_t* const* flags, int32_t world, int32_t rank, uint32_t epoch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,7 @@ from .mixquant import (  # noqa: F401
     DeviceLayer,
     DeviceQuantizedLayer,
     MixedLinearLayer,
+    NcclComm,
     QuantizedModel,
     QuantizedTensor,
     QuantScheme,
@@ -23,6 +24,7 @@ from .mixquant import (  # noqa: F401
     fast_i2f,
     fnv1a_hex,
     pack_nibbles,
+    peer_barrier,
     partition_and_quantize,
     partition_and_quantize_device,
     permute_gathered,

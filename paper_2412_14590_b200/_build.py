@@ -25,7 +25,7 @@ INC = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + os.path.join(CU
 
 CU_SRCS = ["kernels/act_quant.cu", "kernels/mixed_gemm_sm100.cu", "kernels/mixed_gemm_simt.cu",
            "kernels/weight_quant.cu"]
-CPP_SRCS = ["host/mq_host.cpp", "host/mq_layer.cpp"]
+CPP_SRCS = ["host/mq_host.cpp", "host/mq_layer.cpp", "host/mq_nccl.cpp"]
 
 
 def _deps() -> list[str]:

@@ -95,6 +95,14 @@ PROTOTYPES = {
     "mq_layer_create_device": (C.c_int, [C.POINTER(mq_layer_desc), C.POINTER(mq_layer_opts), C.c_int, P,
                                          C.POINTER(P)]),
     "mq_layer_export_packed": (C.c_int, [P, P, C.c_size_t, P]),
+    "mq_nccl_unique_id": (C.c_int, [P]),
+    "mq_nccl_comm_init": (C.c_int, [P, I32, I32, C.c_int, C.POINTER(P)]),
+    "mq_nccl_comm_destroy": (C.c_int, [P]),
+    "mq_mixed_linear_allgather_workspace_bytes": (C.c_size_t, [P, I64, C.POINTER(mq_exec_opts), C.c_int]),
+    "mq_mixed_linear_allgather": (C.c_int, [P, P, C.c_int, I64, P, C.c_int, C.POINTER(mq_exec_opts), P, P, P, P]),
+    "mq_mixed_linear_peers": (C.c_int, [P, P, C.c_int, I64, C.POINTER(P), I32, C.c_int, C.POINTER(mq_exec_opts), P,
+                                        P, P]),
+    "mq_peer_barrier": (C.c_int, [C.POINTER(P), I32, I32, C.c_uint32, P]),
 }
 
 _lib = None

@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "mixllm/capi.h"
 
 struct mq_host_layer_s {
@@ -34,6 +36,9 @@ mq_status check_scheme(const mq_scheme* s);
 mq_status partition_maps(int64_t N, const int32_t* promoted, int64_t np, std::vector<int32_t>& map8,
                          std::vector<int32_t>& map4);
 float round_scale_f16(float s);
+// NCCL binding resolved at run time (mq_nccl.cpp)
+mq_status nccl_check_comm(void* comm, int world, int rank);
+mq_status nccl_all_gather(const void* send, void* recv, size_t count, int dtype, void* comm, cudaStream_t stream);
 
 // proj/include/mixquant/rng.hpp:16-82 (SplitMix64 seeding, xoshiro256++,
 // 53-bit uniforms, Box-Muller normals with a cached spare).

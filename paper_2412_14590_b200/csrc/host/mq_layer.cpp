@@ -39,6 +39,8 @@ struct mq_layer_s {
     double split_span[3] = {0, 0, 0};   // the chosen split's modelled busiest-CTA cost (sub4 groups)
     uint8_t* d_wq = nullptr;
     int32_t* d_colmap = nullptr;
+    int32_t* d_colmap_orig = nullptr;   // sharded layers: original output column of every tile row
+    int32_t* d_shard_colmap = nullptr;  // sharded layers: device copy of shard_colmap (gather permute)
     int64_t bytes_wq = 0, stream_bytes = 0;
     std::vector<TileDesc> tiles;        // host copy (packing / accounting)
     std::vector<int32_t> shard_colmap;  // [world * shard_cols]
@@ -459,6 +461,7 @@ mq_status create_layer(const mq_layer_desc* d, const mq_layer_opts* opts, int de
     const int64_t T = L->tiles8 + L->tiles4;
     L->bytes_wq = (L->tiles8 * kBlock8Bytes + L->tiles4 * kBlock4Bytes) * G;
     std::vector<int32_t> colmap(size_t(std::max<int64_t>(T * kTileRows, 1)), -1);
+    std::vector<int32_t> colmap_orig(o.world > 1 ? colmap.size() : 0, -1);
     L->tiles.resize(size_t(T));
     int64_t coff = 0;
     for (int64_t t = 0; t < T; ++t) {
@@ -475,8 +478,9 @@ mq_status create_layer(const mq_layer_desc* d, const mq_layer_opts* opts, int de
         for (int r = 0; r < rows; ++r) {
             const int64_t srow = (is8 ? a8 : a4) + first + r;  // global sub-problem row
             const int64_t lcol = (is8 ? 0 : L->n8) + first + r;  // local gather column
-            colmap[t * kTileRows + r] = o.world > 1 ? static_cast<int32_t>(lcol)
-                                                    : (is8 ? d->index_map8[srow] : d->index_map4[srow]);
+            const int32_t orig = is8 ? d->index_map8[srow] : d->index_map4[srow];
+            colmap[t * kTileRows + r] = o.world > 1 ? static_cast<int32_t>(lcol) : orig;
+            if (o.world > 1) colmap_orig[t * kTileRows + r] = orig;
         }
         coff += (is8 ? kBlock8Bytes : kBlock4Bytes) * G;
         L->stream_bytes += int64_t(is8 ? kBlock8Bytes : kBlock4Bytes) * G;
@@ -535,6 +539,10 @@ mq_status create_layer(const mq_layer_desc* d, const mq_layer_opts* opts, int de
         e = upload(reinterpret_cast<void**>(&L->d_wq), wq.data(), size_t(L->bytes_wq));
     }
     if (e == cudaSuccess) e = upload(reinterpret_cast<void**>(&L->d_colmap), colmap.data(), colmap.size() * 4);
+    if (e == cudaSuccess && o.world > 1)
+        e = upload(reinterpret_cast<void**>(&L->d_colmap_orig), colmap_orig.data(), colmap_orig.size() * 4);
+    if (e == cudaSuccess && o.world > 1)
+        e = upload(reinterpret_cast<void**>(&L->d_shard_colmap), L->shard_colmap.data(), L->shard_colmap.size() * 4);
     if (e != cudaSuccess) {
         mq_layer_destroy(L);
         return cuda_fail(e, "layer upload");
@@ -688,6 +696,8 @@ void mq_layer_destroy(mq_layer_t L) {
     if (!L) return;
     cudaFree(L->d_wq);
     cudaFree(L->d_colmap);
+    if (L->d_colmap_orig) cudaFree(L->d_colmap_orig);
+    if (L->d_shard_colmap) cudaFree(L->d_shard_colmap);
     if (L->d_ws) cudaFree(L->d_ws);
     for (void* b : L->retired) cudaFree(b);
     delete L;
@@ -755,11 +765,18 @@ size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o
 
 namespace {
 mq_status launch_k2(mq_layer_s* L, const Plan& pl, const void* ws, int64_t M, void* Y, mq_dtype out_dtype,
-                    cudaStream_t s) {
+                    cudaStream_t s, void* const* peers = nullptr, int npeer = 0) {
     const EalWs w = eal_ws_layout(L, pl);
     uint8_t* base = static_cast<uint8_t*>(const_cast<void*>(ws));
     GemmParams p;
     gemm_params(L, pl, M, Y, out_dtype, &p);
+    if (npeer > 0) {  // fused gather: every rank's full Y at the original columns
+        p.npeer = npeer;
+        for (int i = 0; i < npeer; ++i) p.ypeer[i] = peers[i];
+        p.Y = peers[0];
+        p.ldy = L->N;
+        if (L->world > 1) p.colmap = L->d_colmap_orig;
+    }
     p.cnt = reinterpret_cast<uint32_t*>(base);
     p.part = reinterpret_cast<float*>(base + w.off_part);
     p.part2 = reinterpret_cast<float*>(base + w.off_part2);
@@ -862,6 +879,76 @@ mq_status mq_mixed_linear_ws(mq_layer_t L, int64_t M, const void* ws, void* Y, m
     Plan pl;
     if (mq_status st = make_plan(L, M, o, &pl)) return st;
     return launch_k2(L, pl, ws, M, Y, out_dtype, static_cast<cudaStream_t>(stream));
+}
+
+// ------------------------------------------------ column-sharded forwards
+namespace {
+size_t out_size(mq_dtype dt) { return dt == MQ_F32 ? 4 : 2; }
+size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+}  // namespace
+
+size_t mq_mixed_linear_allgather_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o, mq_dtype out_dtype) {
+    const size_t fw = mq_forward_workspace_bytes(L, M, o);
+    if (!fw) return 0;
+    const size_t blk = size_t(M) * size_t(L->shard_cols) * out_size(out_dtype);
+    return al256(fw) + al256(blk) + (L->world > 1 ? al256(blk * size_t(L->world)) : 0);
+}
+
+mq_status mq_mixed_linear_allgather(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t M, void* Y,
+                                    mq_dtype out_dtype, const mq_exec_opts* o, void* ws, int32_t* err, void* comm,
+                                    void* stream) {
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
+    if (!ws) return fail(MQ_USAGE, "the gathered forward needs a workspace (mq_mixed_linear_allgather_workspace_bytes)");
+    if (mq_status st = nccl_check_comm(comm, L->world, L->rank)) return st;
+    if (M == 0) return MQ_OK;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t fw = al256(mq_forward_workspace_bytes(L, M, o));
+    if (fw == 0) return fail(MQ_USAGE, "bad forward options");
+    const size_t blk = size_t(M) * size_t(L->shard_cols);
+    uint8_t* local = static_cast<uint8_t*>(ws) + fw;
+    // this rank's block in gather order, then the gather of every rank's block
+    if (mq_status st = mq_mixed_linear(L, A, a_dtype, M, local, out_dtype, o, ws, err, stream)) return st;
+    if (L->world == 1) return nccl_all_gather(local, Y, blk, out_dtype, comm, s);
+    uint8_t* gathered = local + al256(blk * out_size(out_dtype));
+    if (mq_status st = nccl_all_gather(local, gathered, blk, out_dtype, comm, s)) return st;
+    cudaError_t e = launch_permute(gathered, L->d_shard_colmap, L->world, L->shard_cols, M, L->N, Y, out_dtype, s);
+    if (e != cudaSuccess) return cuda_fail(e, "permute launch");
+    return MQ_OK;
+}
+
+mq_status mq_mixed_linear_peers(mq_layer_t L, const void* A, mq_dtype a_dtype, int64_t M, void* const* y_peers,
+                                int32_t n_peers, mq_dtype out_dtype, const mq_exec_opts* o, void* ws, int32_t* err,
+                                void* stream) {
+    if (!L) return fail(MQ_USAGE, "layer handle is null");
+    if (!y_peers || n_peers < 1 || n_peers > kMaxPeers)
+        return fail(MQ_USAGE, "y_peers must list 1.." + std::to_string(kMaxPeers) + " output buffers");
+    for (int i = 0; i < n_peers; ++i)
+        if (!y_peers[i]) return fail(MQ_USAGE, "null peer output buffer");
+    if (M < 0) return fail(MQ_USAGE, "M must be >= 0");
+    if (M == 0) return MQ_OK;
+    if (a_dtype != MQ_F32 && a_dtype != MQ_F16 && a_dtype != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
+    if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
+    Plan pl;
+    if (mq_status st = make_plan(L, M, o, &pl)) return st;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const EalWs w = eal_ws_layout(L, pl);
+    if (!ws) {
+        if (mq_status st = ensure_internal_ws(L, w.total, s, &ws)) return st;
+    }
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad,
+                                         base + w.off_acts, reinterpret_cast<float*>(base + w.off_sa),
+                                         reinterpret_cast<int32_t*>(base + w.off_asum), err, pl.f16 ? 1 : 0, pl.pdl, s);
+    if (e != cudaSuccess) return cuda_fail(e, "act_quant launch");
+    return launch_k2(L, pl, ws, M, y_peers[0], out_dtype, s, y_peers, n_peers);
+}
+
+mq_status mq_peer_barrier(uint32_t* const* flags, int32_t world, int32_t rank, uint32_t epoch, void* stream) {
+    if (!flags || world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+        return fail(MQ_USAGE, "bad peer barrier arguments");
+    cudaError_t e = launch_peer_barrier(flags, world, rank, epoch, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "peer barrier launch");
+    return MQ_OK;
 }
 
 mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64_t M, int32_t which, int32_t* partials,

@@ -122,4 +122,37 @@ cudaError_t launch_permute(const void* gathered, const int32_t* colmap, int worl
     return cudaGetLastError();
 }
 
+// Cross-rank completion barrier for the fused-gather epilogue: rank `rank`
+// raises its flag in every rank's flag array (release at system scope, so its
+// peer stores are visible first), then waits until every rank's flag in its
+// own array reached `epoch` (acquire). One thread per rank.
+__device__ __forceinline__ void peer_barrier_body(uint32_t* const* flags, int world, int rank, uint32_t epoch) {
+    const int t = threadIdx.x;
+    if (t < world) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags[t] + rank), "r"(epoch) : "memory");
+    __syncthreads();
+    if (t < world) {
+        uint32_t v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags[rank] + t) : "memory");
+            if (int32_t(v - epoch) >= 0) break;
+            __nanosleep(64);
+        }
+    }
+}
+
+struct PeerFlags {
+    uint32_t* f[kMaxPeers];
+};
+__global__ void peer_barrier_kernel_v(PeerFlags pf, int world, int rank, uint32_t epoch) {
+    peer_barrier_body(pf.f, world, rank, epoch);
+}
+
+cudaError_t launch_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, cudaStream_t stream) {
+    if (world < 1 || world > kMaxPeers) return cudaErrorInvalidValue;
+    PeerFlags pf{};
+    for (int i = 0; i < world; ++i) pf.f[i] = flags[i];
+    peer_barrier_kernel_v<<<1, 32, 0, stream>>>(pf, world, rank, epoch);
+    return cudaGetLastError();
+}
+
 }  // namespace mq

@@ -159,10 +159,16 @@ __device__ __forceinline__ void trace_chunk(const GemmParams& p, int ev, int n) 
         p.trace[148 * 8 + ev * 64 + n] = clock64();
 }
 
-__device__ __forceinline__ void store_out(void* Y, int dt, int64_t idx, float v) {
+__device__ __forceinline__ void store_one(void* Y, int dt, int64_t idx, float v) {
     if (dt == 0) static_cast<float*>(Y)[idx] = v;
     else if (dt == 1) static_cast<__half*>(Y)[idx] = __float2half_rn(v);
     else static_cast<__nv_bfloat16*>(Y)[idx] = __float2bfloat16_rn(v);
+}
+// The output element at idx; with the fused gather (npeer > 1, mq_mixed_linear_peers)
+// also into every peer rank's copy of Y at the same (original) column, over NVLink.
+__device__ __forceinline__ void store_out(const GemmParams& p, int64_t idx, float v) {
+    store_one(p.Y, p.out_dtype, idx, v);
+    for (int i = 1; i < p.npeer; ++i) store_one(p.ypeer[i], p.out_dtype, idx, v);
 }
 
 // ring position: slot index + phase parity
@@ -356,7 +362,7 @@ __device__ __noinline__ void split_join_wide(const GemmParams& p, const Work& wk
             if (m < p.M) {
                 float v = v4[e4];
                 if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
+                store_out(p, m * p.ldy + col, v);
             }
         }
     }
@@ -906,7 +912,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                         if (m < p.M) {
                             float v = acc[j];
                             if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                            store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
+                            store_out(p, m * p.ldy + col, v);
                         }
                     }
                 }
@@ -1008,7 +1014,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                         if (m < p.M) {
                             float v = sum[j];
                             if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                            store_out(p.Y, p.out_dtype, m * p.ldy + col, v);
+                            store_out(p, m * p.ldy + col, v);
                         }
                     }
                 }

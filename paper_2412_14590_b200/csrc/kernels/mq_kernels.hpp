@@ -48,6 +48,7 @@ __host__ __device__ inline uint32_t eal_offset(uint32_t m, uint32_t k) {
 // chunk boundaries. Items cut between CTAs are reduced by the piece that
 // completes their G groups (arrival counter counts groups).
 constexpr int kSkMax = 160;  // >= SMs of the device
+constexpr int kMaxPeers = 8;  // ranks of one NVLink domain the fused-gather epilogue writes to
 // Counter words at the start of every forward workspace, indexed by item (a
 // launch with split items has TB == 1, or fewer items than SMs) or by
 // stream-K boundary (<= kSkMax): a fixed region, so one workspace serves any M
@@ -97,6 +98,8 @@ struct GemmParams {
     const uint8_t* pf;      // next layer's packed weights: prefetched into L2 once this launch's reads are issued
     int64_t pf_bytes;       // bytes of pf to prefetch (0: none), split evenly over the CTAs
     int32_t* partials;      // dump mode
+    int32_t npeer;          // fused gather: every output also goes to ypeer[1 .. npeer) (Y == ypeer[0])
+    void* ypeer[kMaxPeers];  // peer ranks' full outputs [M, N] (UVA / NVLink peer-mapped)
     uint32_t skb[kSkMax + 1];  // stream-K CTA boundaries (item << 8 | group)
 };
 
@@ -156,6 +159,8 @@ cudaError_t launch_act_quant_eal(const void* A, int a_dtype, int64_t M, int64_t 
 cudaError_t launch_repack_eal(const int8_t* codes, int64_t ldc, const float* scales, int64_t lds, int per_token,
                               int64_t M, int64_t K, int64_t Mpad, uint8_t* acts, float* sa, int32_t* asum,
                               cudaStream_t stream);
+// Cross-rank completion barrier over peer-mapped flags (mq_peer_barrier).
+cudaError_t launch_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, cudaStream_t stream);
 cudaError_t launch_permute(const void* gathered, const int32_t* colmap, int world, int64_t shard_cols,
                            int64_t M, int64_t N, void* Y, int dtype, cudaStream_t stream);
 

@@ -618,6 +618,38 @@ class DeviceLayer:
         check(lib().mq_mixed_linear_ws(self.h, M, _p(ws), _p(out), _dt(out), C.byref(opts), _stream(stream)))
         return out
 
+    def forward_allgather(self, A, comm: "NcclComm", out=None, out_dtype=None, opts: capi.mq_exec_opts | None = None,
+                          err=None, stream=None):
+        """Column-sharded forward (mq_mixed_linear_allgather): this rank's shard,
+        NCCL all-gather of every rank's block on `comm`, permute to the original
+        column order. Returns the full Y [M, out_features]."""
+        import torch
+        opts = opts or exec_opts()
+        M = A.shape[0]
+        dt = out_dtype or (out.dtype if out is not None else torch.float32)
+        if out is None:
+            out = torch.empty((M, self.info.out_features), dtype=dt, device=A.device)
+        n = lib().mq_mixed_linear_allgather_workspace_bytes(self.h, M, C.byref(opts), _dt(out))
+        key = ("ag", int(n))
+        if key not in self._ws:
+            self._ws[key] = torch.zeros(max(int(n), 16), dtype=torch.uint8, device=A.device)
+        check(lib().mq_mixed_linear_allgather(self.h, _p(A), _dt(A), M, _p(out), _dt(out), C.byref(opts),
+                                              _p(self._ws[key]), _p(err), comm.ptr, _stream(stream)))
+        return out
+
+    def forward_peers(self, A, y_peers, opts: capi.mq_exec_opts | None = None, err=None, stream=None,
+                      workspace=None):
+        """Fused gather (mq_mixed_linear_peers): the epilogue writes this shard's
+        outputs into every tensor of y_peers ([M, out_features] each, one per rank,
+        peer-accessible) at the original columns."""
+        opts = opts or exec_opts()
+        M = A.shape[0]
+        ptrs = (P * len(y_peers))(*[t.data_ptr() for t in y_peers])
+        ws = workspace if workspace is not None else self.workspace(M, opts, True)
+        check(lib().mq_mixed_linear_peers(self.h, _p(A), _dt(A), M, ptrs, len(y_peers), _dt(y_peers[0]),
+                                          C.byref(opts), _p(ws), _p(err), _stream(stream)))
+        return y_peers
+
     def partials(self, codes, which: int, stream=None):
         import torch
         M = codes.shape[0]
@@ -626,6 +658,52 @@ class DeviceLayer:
         out = torch.zeros((G, M, rows), dtype=torch.int32, device=codes.device)
         check(lib().mq_gemm_partials(self.h, _p(codes), codes.stride(0), M, which, _p(out), _stream(stream)))
         return out
+
+
+class NcclComm:
+    """An NCCL communicator for the sharded forwards, bound through the engine's
+    run-time NCCL binding (capi.h: mq_nccl_*). `create` makes a new one from a
+    shared unique id; `from_torch` borrows a torch ProcessGroupNCCL's (the same
+    NCCL library is used, so the handle is valid for the engine)."""
+
+    def __init__(self, ptr, owned: bool):
+        self.ptr = C.c_void_p(ptr) if not isinstance(ptr, C.c_void_p) else ptr
+        self.owned = owned
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().mq_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def create(cls, uid: bytes, world: int, rank: int, device: int) -> "NcclComm":
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib().mq_nccl_comm_init(buf, world, rank, device, C.byref(h)))
+        return cls(h, True)
+
+    @classmethod
+    def from_torch(cls, group=None, device=None) -> "NcclComm":
+        import torch
+        import torch.distributed as dist
+        pg = group or dist.group.WORLD
+        be = pg._get_backend(torch.device("cuda", torch.cuda.current_device() if device is None else device))
+        return cls(be._comm_ptr(), False)
+
+    def __del__(self):
+        if getattr(self, "owned", False) and self.ptr:
+            try:
+                lib().mq_nccl_comm_destroy(self.ptr)
+            except Exception:
+                pass
+            self.owned = False
+
+
+def peer_barrier(flags, world: int, rank: int, epoch: int, stream=None) -> None:
+    """mq_peer_barrier: flags = per-rank uint32 [world] tensors (peer-mapped)."""
+    ptrs = (P * len(flags))(*[t.data_ptr() for t in flags])
+    check(lib().mq_peer_barrier(ptrs, world, rank, epoch, _stream(stream)))
 
 
 def quantize_act(A, group_size: int, ldc: int | None = None, err=None, stream=None, scale_f16: bool = False):

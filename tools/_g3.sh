@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-( time timeout 900 python bench.py --steps 20 --warmup 5 ) > gpurun_out/bench2.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_sharded.py -x -q --timeout 400 > gpurun_out/gputest_sh.log 2>&1; echo rc=$? >> gpurun_out/gputest_sh.log
