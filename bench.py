@@ -8,13 +8,16 @@ proj/src/gemm.cpp:183-192), MQ_FAST mode, fp16 output, batch M (default 16).
 One STEP = the decoder layer's 4 fused projections (qkv, o, gate_up, down), each
 the full dynamic path (activation quantization + mixed GEMM + scatter) = 8 kernel
 launches, replayed from a CUDA graph.
-Synthetic run_bench-generator weights/activations (no checkpoints). Two
-device replicas of the stack (2 x ~128 MB) alternate between steps so the
-weights stream from HBM, not L2 (126 MB).
+Synthetic run_bench-generator weights/activations (no checkpoints). Device
+replicas of the stack (>= 3x the 126 MB L2 of weights per GPU) rotate between
+steps so the weights stream from HBM, not L2.
 
-N > 1 (torchrun): the stack is column-sharded by output feature (each rank
-owns a slice of both the 4-bit and 8-bit partitions), activations replicated,
-outputs all-gathered over NCCL and permuted back: strong scaling.
+N > 1 (--gpus N re-launches itself under torch.distributed.run, or the driver's
+torchrun): the stack is column-sharded by output feature (each rank owns a slice
+of both the 4-bit and 8-bit partitions), activations replicated; each projection
+is ONE engine call, mq_mixed_linear_allgather (shard K1 + K2, ncclAllGather on
+the engine's own communicator, permute back): strong scaling. `kernel_only`
+reports the K2 launches alone.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
 proj/ sources compiled unmodified) on the host cores, same workload, rank 0.
@@ -200,9 +203,9 @@ def run_ours(args):
     for i, (name, N, K) in enumerate(SHAPES_8B):
         W, A, prom = mq.bench_inputs(1, N, K, PERCENT, 1 + i)
         host.append((name, N, K, mq.partition_and_quantize(W, prom, name=name)))
-    stack_bytes = sum(L.sub8.rows * K + L.sub4.rows * K // 2 for (_, _, K, L) in host)
-    # device replicas rotated between steps: >= 3x L2 of weights (L2 hygiene)
-    R = max(3, -(-3 * L2_BYTES // stack_bytes)) if world == 1 else 1
+    stack_bytes = sum(L.sub8.rows * K + L.sub4.rows * K // 2 for (_, _, K, L) in host) // world  # per rank
+    # device replicas rotated between steps: >= 3x L2 of weights per GPU (L2 hygiene)
+    R = max(3, -(-3 * L2_BYTES // stack_bytes))
     reps = [mq.DeviceLayer.replicas(L, R, local, rank=rank, world=world) for (_, _, _, L) in host]
     layers = [[reps[i][r] for i in range(len(host))] for r in range(R)]
     mode = capi.MQ_FAST if args.mode == "fast" else capi.MQ_EXACT
@@ -214,17 +217,22 @@ def run_ours(args):
         opts = mq.exec_opts(mode, act_group)
         return xs, ys, opts
 
-    colmaps, gathered, finals = None, None, None
+    comm, finals = None, None
     if world > 1:
-        colmaps = [torch.from_numpy(layers[0][i].shard_colmap()).to(dev) for i in range(len(host))]
+        # the engine's own communicator (capi.h mq_nccl_*): rank 0's unique id,
+        # broadcast over the torch process group
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(mq.NcclComm.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = mq.NcclComm.create(bytes(uid.cpu().numpy()), world, rank, local)
 
     def step(r, xs, ys, opts, m):
         for i in range(len(host)):
-            layers[r][i].forward(xs[i], out=ys[i], opts=opts)
-            if world > 1:
-                dist.all_gather_into_tensor(gathered[i], ys[i])
-                mq.permute_gathered(gathered[i], colmaps[i], world, layers[r][i].out_cols, m, host[i][1],
-                                    out=finals[i])
+            if world > 1:  # shard K1 + K2, ncclAllGather, permute: one engine call (mq_mixed_linear_allgather)
+                layers[r][i].forward_allgather(xs[i], comm, out=finals[i], opts=opts)
+            else:
+                layers[r][i].forward(xs[i], out=ys[i], opts=opts)
 
     def step_k2(r, wss, ys, opts, m):
         for i in range(len(host)):
@@ -254,16 +262,10 @@ def run_ours(args):
 
     def bench_batch(m, act_group, steps, warmup, sampler=None, mode=mode):
         xs, ys, opts = make_io(m, act_group, mode)
-        nonlocal gathered, finals
+        nonlocal finals
         if world > 1:
-            gathered = [torch.empty((world, m, layers[0][i].out_cols), dtype=torch.float16, device=dev)
-                        for i in range(len(host))]
             finals = [torch.empty((m, host[i][1]), dtype=torch.float16, device=dev) for i in range(len(host))]
-            fns = [lambda r=r: step(r, xs, ys, opts, m) for r in range(R)]  # eager (NCCL)
-            for f in fns:
-                f()
-        else:
-            fns = graphs_for(lambda r: step(r, xs, ys, opts, m))
+        fns = graphs_for(lambda r: step(r, xs, ys, opts, m))  # NCCL kernels are graph-capturable
 
         def ramp():  # pre-ramp clocks (not counted as steps)
             t_end = time.time() + 0.3
@@ -280,9 +282,8 @@ def run_ours(args):
             ms = timed(fns, steps, warmup)
         # K2-only timing (the dominant kernel), same graphs minus K1
         wss = [[layers[r][i].quantize_ws(xs[i], opts) for i in range(len(host))] for r in range(R)]
-        k2fns = graphs_for(lambda r: step_k2(r, wss, ys, opts, m)) if world == 1 else \
-            [lambda r=r: step_k2(r, wss, ys, opts, m) for r in range(R)]
-        ms_k2 = timed(k2fns, steps, warmup)
+        k2fns = graphs_for(lambda r: step_k2(r, wss, ys, opts, m))
+        ms_k2 = timed(k2fns, steps, warmup)  # kernel only (no gather): the north_star's scaling figure
         ops = sum(2.0 * m * N * K for (_, N, K, _) in host)
         b2 = sum(k2_bytes(m, N // world if world > 1 else N, K, L.sub8.rows // world, L.sub4.rows // world)
                  for (_, N, K, L) in host)
@@ -321,8 +322,9 @@ def run_ours(args):
 
     # ---- e2e through the public C-ABI path with host buffers (pinned), N GPUs
     e2e = None
-    if world == 1:
-        xs, ys = head["xs"], head["ys"]
+    if True:
+        xs = head["xs"]
+        ys = [torch.empty((M, N), dtype=torch.float16, device=dev) for (_, N, _, _) in host]  # full outputs
         # one pinned input buffer (every layer's activations) and one output
         # buffer: one H2D and one D2H copy per step
         nx = [x.numel() for x in xs]
@@ -360,7 +362,10 @@ def run_ours(args):
                     ready.append(ev)
             for i in range(len(host)):
                 main.wait_event(ready[i])
-                layers[r][i].forward(xv[i], out=yv[i], opts=head["opts"])
+                if world > 1:
+                    layers[r][i].forward_allgather(xv[i], comm, out=yv[i], opts=head["opts"])
+                else:
+                    layers[r][i].forward(xv[i], out=yv[i], opts=head["opts"])
                 done = torch.cuda.Event()
                 done.record(main)
                 s_out.wait_event(done)
@@ -451,18 +456,22 @@ def run_ours(args):
                                    f"A8 group-wise (reference semantics); mode {args.mode}; fp16 out",
                        "batch": M, "group": GROUP, "percent_8bit": PERCENT,
                        "parallelism": f"column-shard x{world}" if world > 1 else "single",
-                       "l2": f"{R} device replicas of the stack ({R * stack_bytes / 2**20:.0f} MB of weights, "
+                       "l2": f"{R} device replicas of the stack ({R * stack_bytes / 2**20:.0f} MB of weights per GPU, "
                              f">= 3x the 126 MB L2) rotate between steps",
-                       "cuda_graph": world == 1},
+                       "cuda_graph": True},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": k2_traffic(M),
                          "kernel": f"mixed_gemm_tc_kernel ({len(SHAPES_8B)} launches/step; bytes and time summed)",
                          "peak_kind": peak_kind,
                          "k2_bytes_per_step": int(head["k2_bytes"]), "k2_ms_per_step": round(head["ms_k2"], 5),
                          "per_layer": per_layer},
+            "kernel_only": {"value": round(head["ops"] / (head["ms_k2"] * 1e-3) / 1e12, 3), "unit": "TOPS",
+                            "ms_per_step": round(head["ms_k2"], 5),
+                            "what": "the 4 K2 launches per step, no activation quantization and no gather "
+                                    "(the north_star's kernel-only scaling figure)"},
             "int8_peak_tops_measured": round(int8_peak, 1) if int8_peak else None,
             "int8_peak_tops_spec": INT8_SPEC_TOPS,
-            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps * 2 * len(SHAPES_8B), "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": args.steps * (2 if world == 1 else 3) * len(SHAPES_8B), "clocks": clocks,
             "sweep": sweep,
             "c1": c1,
             "c3_70b": c3,
@@ -629,6 +638,24 @@ def k2_traffic(m):
         return None
 
 
+def self_launch(args) -> bool:
+    """bench.py --gpus N outside torchrun: re-run under torch.distributed.run
+    with N ranks on this node (127.0.0.1 rendezvous). Returns True if it did."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -642,6 +669,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-70b", action="store_true")
     args = ap.parse_args()
+    if self_launch(args):
+        return
     if args.impl == "reference":
         run_reference(args)
     else:
