@@ -23,8 +23,8 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INC = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + os.path.join(CUDA, "include")]
 
-CU_SRCS = ["kernels/act_quant.cu", "kernels/mixed_gemm_sm100.cu", "kernels/mixed_gemm_simt.cu",
-           "kernels/weight_quant.cu"]
+CU_SRCS = ["kernels/act_quant.cu", "kernels/mixed_gemm_sm100.cu", "kernels/mixed_gemm_peers.cu",
+           "kernels/mixed_gemm_simt.cu", "kernels/weight_quant.cu"]
 CPP_SRCS = ["host/mq_host.cpp", "host/mq_layer.cpp", "host/mq_nccl.cpp"]
 
 
@@ -57,15 +57,19 @@ def build(verbose: bool = False, force: bool = False, defines: tuple = (), lib: 
     obj_dir = obj or OBJ
     os.makedirs(obj_dir, exist_ok=True)
     deps = _deps()
-    objs = []
+    objs, jobs = [], []
     for src in CU_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(obj_dir, os.path.basename(src) + ".o")
         objs.append(o)
         if force or _stale(o, [s] + deps):
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *defines,
-                  "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
-                  *INC, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *defines,
+                         "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
+                         *INC, "-c", s, "-o", o])
+    if jobs:  # the kernel translation units compile in parallel
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(len(jobs)) as ex:
+            list(ex.map(_run, jobs))
     for src in CPP_SRCS:
         s = os.path.join(CSRC, src)
         o = os.path.join(obj_dir, os.path.basename(src) + ".o")
