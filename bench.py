@@ -626,10 +626,10 @@ def run_reference(args):
 
 def k2_traffic(m):
     """DRAM bytes (read + write) per step of the K2 launches from the committed ncu
-    launch list of this workload (profiles/r1/k2_traffic.json, written by
+    launch list of this workload (profiles/r2/k2_traffic.json, written by
     tools/launch_summary.py from `ncu --metrics dram__bytes_*`); None when absent
     or for another batch."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "k2_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r2", "k2_traffic.json")
     if m != 16 or not os.path.exists(path):
         return None
     try:

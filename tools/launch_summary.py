@@ -23,7 +23,6 @@ print("`ncu --metrics gpu__time_duration.sum --clock-control none -c 400` — co
       "(no PDL overlap), so compare SHARES, not absolute times.\n")
 print("One step = 4 x (K1 act_quant_eal + K2 mixed_gemm) for qkv (6144x4096), o (4096x4096), "
       "gate_up (28672x4096), down (4096x14336), M=16.\n")
-print("| # | kernel | grid | us |\n|---|---|---|---|")
 tot = k2 = 0.0
 traffic = 0.0
 has_dram = all("dram__bytes_read.sum" in r for r in step)
