@@ -247,8 +247,9 @@ typedef struct {
     int32_t token_tile;  /* 0 = auto; else 16/32/64/128 */
     int32_t gemm_impl;   /* 0 = tcgen05 (product); 1 = SIMT debug kernel */
     int32_t no_pdl;      /* 1 = plain launches (default: programmatic dependent launch) */
-    int32_t schedule;    /* MQ_FAST token-tiled launches: 0 = auto, 1 = unit rounds, 2 = stream-K
-                            (equal work per SM; each cut item summed head + tail) where it applies */
+    int32_t schedule;    /* MQ_FAST: 0 = auto (prefill: stream-K where the unit rounds leave SMs idle;
+                            decode: unit schedule), 1 = unit rounds, 2 = stream-K wherever it applies,
+                            decode included (equal work per SM; a cut item is joined by its last piece) */
     int32_t concurrent;  /* 1 = other kernels may hold SMs during this launch (multi-stream use,
                             overlapped collectives): never use a schedule whose CTAs wait on each
                             other (the one-round wide-tile barrier join); 0 = the launch owns the

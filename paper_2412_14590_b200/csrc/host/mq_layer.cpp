@@ -340,10 +340,14 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dty
         p->pf = pl.pf_layer->d_wq;
         p->pf_bytes = std::min<int64_t>(cap, pl.pf_layer->bytes_wq) / 256 * 256;
     }
-    static const int dbg = [] {
+#ifdef MQ_DEV
+    static const int dbg = [] {  // development builds: pipeline-stage bypass / trace bits
         const char* e = std::getenv("MQ_DBG");
         return e ? std::atoi(e) : 0;
     }();
+#else
+    constexpr int dbg = 0;
+#endif
     p->dbg = dbg;
     if (dbg & 32) {
         static unsigned long long* tr = [] {
@@ -1002,13 +1006,16 @@ mq_status mq_gemm_partials(mq_layer_t L, const int8_t* codes, int64_t ldc, int64
     return MQ_OK;
 }
 
-// development: copy the last traced launch's per-CTA timestamps (MQ_DBG & 32)
+#ifdef MQ_DEV
+// development builds only (-DMQ_DEV, tools/trace_k2.py): copy the last traced
+// launch's per-CTA timestamps (MQ_DBG & 32); not part of the C ABI
 int mq_debug_trace(unsigned long long* out) {
     if (!g_trace_buf) return 0;
     cudaDeviceSynchronize();
     cudaMemcpy(out, g_trace_buf, (148 * 8 + 1024) * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     return 148;
 }
+#endif
 
 mq_status mq_permute_gathered(const void* gathered, const int32_t* colmap, int32_t world, int64_t sc, int64_t M,
                               int64_t N, void* Y, mq_dtype dt, void* stream) {
