@@ -347,25 +347,41 @@ def run_ours(args):
         dyf = list(torch.split(dy_all, ny))
         s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
+        # The first input and the last output are on the step's critical path, and a
+        # copy-engine transfer inside a graph carries several us of scheduling
+        # latency (tools/e2e_probe.py: 110 -> 96 us per step): K1 of the first
+        # projection quantizes its activations straight from pinned host memory
+        # (a UVA view, read over PCIe), and a copy kernel writes the last output to
+        # pinned host memory; the other transfers run on the copy engines,
+        # overlapped with the other projections' kernels.
+        x0_host = mq.pinned_view(hxv[0].view(xs[0].shape))
+        y_last_host = mq.pinned_view(hyv[-1].view(ys[-1].shape))
+
         def e2e_step(r):
             main = torch.cuda.current_stream(dev)
             fork = torch.cuda.Event()
             fork.record(main)
             s_in.wait_event(fork)
             s_out.wait_event(fork)
-            ready = []
+            ready = [None]
             with torch.cuda.stream(s_in):
-                for i in range(len(host)):
+                for i in range(1, len(host)):
                     dxf[i].copy_(hxv[i], non_blocking=True)
                     ev = torch.cuda.Event()
                     ev.record(s_in)
                     ready.append(ev)
+            last = len(host) - 1
             for i in range(len(host)):
-                main.wait_event(ready[i])
+                if ready[i] is not None:
+                    main.wait_event(ready[i])
+                x = x0_host if i == 0 else xv[i]
                 if world > 1:
-                    layers[r][i].forward_allgather(xv[i], comm, out=yv[i], opts=head["opts"])
+                    layers[r][i].forward_allgather(x, comm, out=yv[i], opts=head["opts"])
                 else:
-                    layers[r][i].forward(xv[i], out=yv[i], opts=head["opts"])
+                    layers[r][i].forward(x, out=yv[i], opts=head["opts"])
+                if i == last:
+                    torch.add(yv[i], 0, out=y_last_host)  # device -> pinned host, over PCIe
+                    continue
                 done = torch.cuda.Event()
                 done.record(main)
                 s_out.wait_event(done)
@@ -382,7 +398,10 @@ def run_ours(args):
             efns[0]()
             torch.cuda.synchronize()
         ems = timed(efns, args.steps, args.warmup)
-        e2e = {"value": head["ops"] / (ems * 1e-3) / 1e12, "unit": "TOPS",
+        # the host output buffer holds what the device-resident step computes
+        ref_out = torch.cat([y.reshape(-1).cpu() for y in head["ys"]]) if world == 1 else None
+        same = bool(torch.equal(hy_all, ref_out)) if ref_out is not None else None
+        e2e = {"value": head["ops"] / (ems * 1e-3) / 1e12, "unit": "TOPS", "host_output_matches_device": same,
                "h2d_bytes_per_step": int(hx_all.numel() * 4),
                "d2h_bytes_per_step": int(hy_all.numel() * 2), "ms_per_step": ems}
 

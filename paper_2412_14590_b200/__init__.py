@@ -28,6 +28,7 @@ from .mixquant import (  # noqa: F401
     partition_and_quantize,
     partition_and_quantize_device,
     permute_gathered,
+    pinned_view,
     prepack_weights,
     quantize_act,
     quantize_tensor,

@@ -244,6 +244,22 @@ def _device_view(ptr, nbytes: int, device: int):
         return torch.as_tensor(_Arr(), device=f"cuda:{device}")
 
 
+def pinned_view(t):
+    """A CUDA tensor aliasing a pinned host tensor (UVA): the engine's kernels read
+    or write it over PCIe directly — e.g. K1 quantizing activations straight from
+    pinned host memory, with no copy-engine transfer in between."""
+    import torch
+    if t.is_cuda or not t.is_pinned():
+        raise UsageError("pinned_view expects a pinned host tensor")
+    typestr = {torch.float32: "<f4", torch.float16: "<f2", torch.bfloat16: "<V2", torch.uint8: "|u1"}[t.dtype]
+
+    class _A:
+        __cuda_array_interface__ = {"shape": tuple(t.shape), "typestr": typestr, "data": (t.data_ptr(), False),
+                                    "version": 3, "strides": None}
+    v = torch.as_tensor(_A(), device=f"cuda:{torch.cuda.current_device()}")
+    return v.view(t.dtype) if t.dtype == torch.bfloat16 else v
+
+
 def partition_and_quantize_device(weight, promoted, largebit: QuantScheme = LARGEBIT,
                                   smallbit: QuantScheme = SMALLBIT, name: str = "",
                                   stream=None) -> DeviceQuantizedLayer:
