@@ -838,13 +838,25 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                     const float* sav = msw + C::kMetaSa + j * BN + c0;
                     const float2 sw2 = pk2(sw, sw);
                     const uint32_t tcol = uint32_t((rt.idx * GPS + j) * BN + c0);
-                    constexpr int CW = BNE < 16 ? BNE : 16;  // TMEM columns per load
+#ifndef MQ_CW64
+#define MQ_CW64 64
+#endif
+                    // TMEM columns per tcgen05.wait::ld: two 16-column loads in flight per wait
+                    // for 128-token tiles (register budget: 32 keeps 128 registers without spills;
+                    // M = 512 stack -5%, M = 256 -2.5%), MQ_CW64 for 64-token tiles (64: -0.7..2% at M 33-64)
+                    constexpr int CW = BNE < 16 ? BNE : (BN == 64 ? MQ_CW64 : (BNE >= 32 ? 32 : 16));
 #pragma unroll
                     for (int ch = 0; ch < BNE / CW; ++ch) {
                         if (dbg_bits(p) & 1) break;
                         uint32_t v[CW];
-                        if constexpr (CW == 16) ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * 16, v);
-                        else ptx::tmem_ld8(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * CW, v);
+                        if constexpr (CW >= 16) {
+#pragma unroll
+                            for (int h = 0; h < CW / 16; ++h)
+                                ptx::tmem_ld16(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * CW + h * 16,
+                                               *reinterpret_cast<uint32_t(*)[16]>(v + h * 16));
+                        } else {
+                            ptx::tmem_ld8(tmem_base + (uint32_t(wq * 32) << 16) + tcol + ch * CW, v);
+                        }
                         ptx::tmem_wait_ld();
                         if constexpr (C::kZpEpi) {  // S = sum a c - z sum a (exact int32)
                             const int32_t zr = reinterpret_cast<const int32_t*>(msw)[C::kMetaZp + j * 128 + r];
@@ -864,15 +876,19 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                             }
                         } else if constexpr (kPair) {
 #pragma unroll
-                            for (int q = 0; q < CW; q += 2) {
+                            for (int q = 0; q < CW; q += 4) {
                                 const int jj = ch * CW + q;
-                                // exact int -> f32 (|S| < 2^22), two lanes per FFMA2
-                                const float2 g2 = pk2(__int2float_rn(int32_t(v[q])), __int2float_rn(int32_t(v[q + 1])));
+                                // exact int -> f32 (|S| < 2^22), two lanes per FFMA2; four
+                                // activation scales per 16-byte shared load
+                                const float2 g2a = pk2(__int2float_rn(int32_t(v[q])), __int2float_rn(int32_t(v[q + 1])));
+                                const float2 g2b = pk2(__int2float_rn(int32_t(v[q + 2])), __int2float_rn(int32_t(v[q + 3])));
                                 if constexpr (MODE == kFastGroup) {
-                                    const float2 sa2 = *reinterpret_cast<const float2*>(sav + jj);
-                                    acc2[jj / 2] = fma2(g2, mul2(sa2, sw2), acc2[jj / 2]);
+                                    const float4 sa4 = *reinterpret_cast<const float4*>(sav + jj);
+                                    acc2[jj / 2] = fma2(g2a, mul2(make_float2(sa4.x, sa4.y), sw2), acc2[jj / 2]);
+                                    acc2[jj / 2 + 1] = fma2(g2b, mul2(make_float2(sa4.z, sa4.w), sw2), acc2[jj / 2 + 1]);
                                 } else {
-                                    acc2[jj / 2] = fma2(g2, sw2, acc2[jj / 2]);
+                                    acc2[jj / 2] = fma2(g2a, sw2, acc2[jj / 2]);
+                                    acc2[jj / 2 + 1] = fma2(g2b, sw2, acc2[jj / 2 + 1]);
                                 }
                             }
                         } else {

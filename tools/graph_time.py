@@ -14,7 +14,7 @@ for (N, K) in SH:
     L = mq.partition_and_quantize(W, prom)
     reps = [mq.DeviceLayer(L) for _ in range(2)]
     dA = torch.from_numpy(A).cuda()
-    opts = mq.exec_opts(capi.MQ_FAST, 128, ksplit=int(os.environ.get("KSPLIT", "0")), schedule=int(os.environ.get("SCHED", "0")), pdl=os.environ.get("NOPDL") is None)
+    opts = mq.exec_opts(capi.MQ_FAST, 128, ksplit=int(os.environ.get("KSPLIT", "0")), schedule=int(os.environ.get("SCHED", "0")), pdl=os.environ.get("NOPDL") is None, token_tile=int(os.environ.get("TT", "0")))
     wss = [r.quantize_ws(dA, opts) for r in reps]
     Y = torch.empty((M, N), dtype=torch.float16, device="cuda")
     for i in range(4):
