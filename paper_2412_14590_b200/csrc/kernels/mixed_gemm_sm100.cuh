@@ -78,11 +78,23 @@ struct TcCfg {
     static constexpr int kXStageBytes = ((kOffAs + (kZpEpi ? GPS * BN * 4 : 0)) + 1023) / 1024 * 1024;
     // activation stages: a prefill tile needs a fresh 16 KB activation tile per
     // group (from L2), so its ring is as deep as the weight ring
-    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? 6 : (kDec && BN == 16) ? 4 : 3;
+    #ifndef MQ_NX16
+#define MQ_NX16 8
+#endif
+#ifndef MQ_NX32
+#define MQ_NX32 3
+#endif
+    // (16-token tiles: 8 activation stages and 3 weight stages beat 3 + 5 — the
+    // activations come from L2 under full HBM streaming, so their ring needs the
+    // depth; M <= 16 stack -2%. 32-token tiles: 3 — 6 was 9% slower)
+    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? 6 : BN == 16 ? MQ_NX16 : MQ_NX32;
     // TMEM rings: NT accumulator chunk slots of GPS x BN int32 columns, NA
     // A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
-    static constexpr int NT = BN >= 128 ? 3 : 2;
+#ifndef MQ_NT16
+#define MQ_NT16 2
+#endif
+    static constexpr int NT = BN >= 128 ? 3 : BN == 16 ? MQ_NT16 : 2;
     static constexpr int NA0 = int((kTmemBudget - NT * kAccPerChunk) / kAPerChunk);
     static constexpr int NA = NA0 > 4 ? 4 : NA0;
     static constexpr uint32_t kAccCols = NT * kAccPerChunk;
