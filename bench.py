@@ -156,6 +156,17 @@ SHAPES_70B = [("qkv_proj", 8192 + 1024 + 1024, 8192), ("o_proj", 8192, 8192),
 SWEEP_M = (1, 16, 64, 256, 512)
 
 
+def workload_config(M: int, world: int = 1) -> dict:
+    """The `config` both arms report (the same workload: same shapes, batch, 8-bit
+    fraction, schemes and activation semantics); how each arm computes it
+    (precision mode, output dtype, replicas, graphs) is in `impl_detail`."""
+    return {"workload": f"llama3.1-8b decoder-layer linear stack (fused qkv 6144x4096, o 4096x4096, fused gate_up "
+                        f"28672x4096, down 4096x14336); batch {M}; {int(PERCENT * 100)}% 8-bit output features; "
+                        f"W4 g128 asym + W8 sym; A8 group-wise (reference semantics)",
+            "batch": M, "group": GROUP, "percent_8bit": PERCENT,
+            "parallelism": f"column-shard x{world}" if world > 1 else "single"}
+
+
 def graph_of(torch, fn):
     """fn() captured into a CUDA graph (after one eager warm-up call)."""
     fn()
@@ -470,14 +481,11 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int8 (int32 accum, f32 rescale, f16 out)",
             "data": "synthetic (run_bench generator weights, randn activations)",
-            "config": {"workload": f"llama3.1-8b decoder-layer linear stack (fused qkv 6144x4096, o 4096x4096, fused gate_up 28672x4096, down 4096x14336); batch {M}; "
-                                   f"{int(PERCENT * 100)}% 8-bit output features; W4 g128 asym + W8 sym; "
-                                   f"A8 group-wise (reference semantics); mode {args.mode}; fp16 out",
-                       "batch": M, "group": GROUP, "percent_8bit": PERCENT,
-                       "parallelism": f"column-shard x{world}" if world > 1 else "single",
-                       "l2": f"{R} device replicas of the stack ({R * stack_bytes / 2**20:.0f} MB of weights per GPU, "
-                             f">= 3x the 126 MB L2) rotate between steps",
-                       "cuda_graph": True},
+            "config": workload_config(M, world),
+            "impl_detail": {"mode": args.mode, "out_dtype": "fp16",
+                            "l2": f"{R} device replicas of the stack ({R * stack_bytes / 2**20:.0f} MB of weights per "
+                                  f"GPU, >= 3x the 126 MB L2) rotate between steps",
+                            "cuda_graph": True},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": k2_traffic(M),
                          "kernel": f"mixed_gemm_tc_kernel ({len(SHAPES_8B)} launches/step; bytes and time summed)",
@@ -631,10 +639,9 @@ def run_reference(args):
             "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": budget_steps, "warmup": min(args.warmup, 1),
             "ms_per_step": res.get("ms_per_step"), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int8 (int32 accum, f32 rescale, f32 out)", "data": "synthetic",
-            "config": {"workload": f"llama3.1-8b decoder-layer linear stack (fused qkv 6144x4096, o 4096x4096, fused gate_up 28672x4096, down 4096x14336); batch {args.batch}; "
-                                   f"{int(PERCENT * 100)}% 8-bit output features; W4 g128 asym + W8 sym; "
-                                   f"A8 group-wise (reference semantics); reference CPU path",
-                       "batch": args.batch},
+            "config": workload_config(args.batch, int(os.environ.get("WORLD_SIZE", "1"))),
+            "impl_detail": {"path": "the reference's own execute_mixed_linear (oracle/_ref, proj/src compiled "
+                                    "unmodified) on the host cores", "mode": "exact (reference)", "out_dtype": "f32"},
             "cpu_baseline": {"value": res["value"], "unit": "TOPS", "cores": res["cores"], "kind": res["kind"],
                              "sample": res["sample"]},
             "e2e": {"value": res["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
