@@ -248,11 +248,8 @@ typedef struct {
     int32_t gemm_impl;   /* 0 = tcgen05 (product); 1 = SIMT debug kernel */
     int32_t no_pdl;      /* 1 = plain launches (default: programmatic dependent launch) */
     int32_t schedule;    /* MQ_FAST: 0 = auto (prefill: stream-K where the unit rounds leave SMs idle;
-                            decode: unit rounds), 1 = unit rounds, 2 = stream-K wherever it applies, decode included
-                            (equal work per SM; a cut item is joined by its last piece), 3 = the hybrid
-                            decode schedule (whole sub4 tiles one per SM first, then an equal stream-K
-                            share of the rest) where the layer has enough tiles; 2 and 3 are correct
-                            but measured slower than unit rounds on the Llama decode shapes */
+                            decode: unit schedule), 1 = unit rounds, 2 = stream-K wherever it applies,
+                            decode included (equal work per SM; a cut item is joined by its last piece) */
     int32_t concurrent;  /* 1 = other kernels may hold SMs during this launch (multi-stream use,
                             overlapped collectives): never use a schedule whose CTAs wait on each
                             other (the one-round wide-tile barrier join); 0 = the launch owns the

@@ -73,7 +73,6 @@ int auto_token_tile(int64_t M) {
 
 struct Plan {
     int bn, tb, mode, per_token, S4, S8, units, grid;
-    int hyb = 0, T2 = 0;  // hybrid decode schedule: whole-tile rounds, stream-K tiles [0, T2)
     int64_t Mpad;
     bool pdl, rotate, sk, no_spin, f16;
     const mq_layer_s* pf_layer;
@@ -109,36 +108,8 @@ bool stream_k_pays(const mq_layer_s* L, const Plan* pl, bool force) {
 // So the unit schedule stays the default and schedule = 2 forces stream-K.
 bool decode_stream_k_pays(const mq_layer_s*, bool force) { return force; }
 
-// Hybrid decode schedule (the Stream-K paper's "data-parallel + stream-K"):
-// R1 rounds of whole sub4 tiles, one per CTA per round and never cut, THEN an
-// equal stream-K share of the remaining tiles (all sub8 tiles and the other
-// sub4 tiles) per CTA. Every cut item is joined at the end of a CTA's work,
-// so — unlike the pure decode stream-K — no join stalls a CTA that still has
-// whole tiles to stream. It pays where the power-of-two unit splits cannot
-// balance (gate_up 28672x4096: busiest CTA 64 -> ~54 group-units) — in the
-// model. Measured, it is slower (gate_up 21.4 vs 19.0 us: the cut tiles' joins
-// at the end of every CTA cost more than the balance gains), so it is opt-in
-// (schedule = 3). Returns R1 (0: not used) and the stream-K tile count.
-int decode_hybrid_rounds(const mq_layer_s* L, bool force, int* T2) {
-    const int grid = std::min<int>(L->num_sms, kSkMax);
-    const double G = double(L->G);
-    const double C = double(L->tiles8) * 2.0 * G + double(L->tiles4) * G;
-    int R1 = static_cast<int>(std::min<double>(double(L->tiles4 / grid), std::floor(C / grid / G)));
-    if (R1 < 1) return 0;
-    const double C2 = C - double(R1) * grid * G;
-    if (C2 <= 0) return 0;
-    const double span = R1 * G + C2 / grid + gemm_gps(16) + 2 * 2.0 + 4.0;  // best_split's cost model
-    if (!force && span >= L->split_span[0] - 1e-9) return 0;
-    *T2 = static_cast<int>(L->tiles8 + L->tiles4 - int64_t(R1) * grid);
-    return R1;
-}
-
-// items_limit (hybrid decode schedule, tb == 1): the ranges cover tiles
-// [0, items_limit) only; the remaining tiles are phase 1 (whole, one per CTA).
-void plan_stream_k(const mq_layer_s* L, Plan* pl, int64_t items_limit = -1) {
-    const int64_t G = L->G, T = L->tiles8 + L->tiles4;
-    const int64_t Tl = items_limit < 0 ? T : items_limit;
-    const int64_t T8 = std::min<int64_t>(L->tiles8, Tl), T4 = Tl - T8;
+void plan_stream_k(const mq_layer_s* L, Plan* pl) {
+    const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4, T = T8 + T4;
     const int64_t c8 = pl->bn <= 32 ? 2 : 1;
     const int gps = gemm_gps(pl->bn), gps8 = gps / 2 > 0 ? gps / 2 : 1;
     const int64_t ctb = T8 * G * c8 + T4 * G, total = ctb * pl->tb;
@@ -161,7 +132,7 @@ void plan_stream_k(const mq_layer_s* L, Plan* pl, int64_t items_limit = -1) {
         }
         pl->skb[b] = static_cast<uint32_t>(((tb * T + t) << 8) | g);
     }
-    pl->skb[grid] = static_cast<uint32_t>(items_limit < 0 ? (int64_t(pl->tb) * T) << 8 : Tl << 8);
+    pl->skb[grid] = static_cast<uint32_t>((int64_t(pl->tb) * T) << 8);
     // chunk rounding can make neighbouring boundaries equal: drop the empty
     // ranges, so the boundaries are strictly increasing (the decode join finds
     // an item's pieces as the CTAs between two boundary searches)
@@ -289,33 +260,20 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     pl->grid = std::min(pl->units, L->num_sms);
     pl->sk = false;
     // stream-K when the unit schedule's last round would leave CTAs idle
-    if (o->schedule < 0 || o->schedule > 3)
-        return fail(MQ_USAGE, "schedule must be 0 (auto), 1 (units), 2 (stream-K) or 3 (hybrid decode)");
+    if (o->schedule < 0 || o->schedule > 2) return fail(MQ_USAGE, "schedule must be 0 (auto), 1 (units) or 2 (stream-K)");
     const int64_t items = int64_t(pl->tb) * (L->tiles8 + L->tiles4);
     if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn >= 64 && pl->S4 == 1 && pl->S8 == 1 && L->G < 256 &&
         items * 256 < (int64_t(1) << 32) &&
         o->schedule != 1 && stream_k_pays(L, pl, o->schedule == 2))
         plan_stream_k(L, pl);
-    if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn <= 32 && pl->tb == 1 && L->G < 256 && o->schedule != 1) {
-        int T2 = 0, R1 = 0;
-        if (o->schedule == 3 && (R1 = decode_hybrid_rounds(L, true, &T2)) > 0) {
-            Plan h = *pl;
-            plan_stream_k(L, &h, T2);
-            // phase 1 maps tile T2 + b + k * grid to CTA b: needs the full grid
-            if (h.grid == std::min<int>(L->num_sms, kSkMax)) {
-                *pl = h;
-                pl->hyb = R1;
-                pl->T2 = T2;
-            }
-        } else if (decode_stream_k_pays(L, o->schedule == 2)) {
-            plan_stream_k(L, pl);
-        }
-    }
+    if (o->mode == MQ_FAST && o->ksplit == 0 && pl->bn <= 32 && pl->tb == 1 && L->G < 256 && o->schedule != 1 &&
+        decode_stream_k_pays(L, o->schedule == 2))
+        plan_stream_k(L, pl);
     static const bool plan_log = std::getenv("MQ_PLAN_LOG") != nullptr;  // development
     if (plan_log)
-        std::fprintf(stderr, "mq plan: N=%lld K=%lld M=%lld bn=%d tb=%d S4=%d S8=%d units=%d grid=%d sk=%d hyb=%d T2=%d\n",
+        std::fprintf(stderr, "mq plan: N=%lld K=%lld M=%lld bn=%d tb=%d S4=%d S8=%d units=%d grid=%d sk=%d\n",
                      (long long)L->N, (long long)L->K, (long long)M, pl->bn, pl->tb, pl->S4, pl->S8, pl->units, pl->grid,
-                     pl->sk ? 1 : 0, pl->hyb, pl->T2);
+                     pl->sk ? 1 : 0);
     return MQ_OK;
 }
 
@@ -373,8 +331,6 @@ void gemm_params(const mq_layer_s* L, const Plan& pl, int64_t M, void* Y, mq_dty
     p->rotate = pl.rotate ? 1 : 0;
     p->T = static_cast<int32_t>(L->tiles8 + L->tiles4);
     p->sk = pl.sk ? 1 : 0;
-    p->hyb = pl.hyb;
-    p->T2 = pl.T2;
     if (pl.sk) std::copy(pl.skb.begin(), pl.skb.end(), p->skb);
     p->idesc8 = idesc_i8(0, L->w8_mode == MQ_W8_SIGNED, true);
     if (pl.pf_layer && pl.pf_layer != L && pl.pf_layer->device == L->device) {

@@ -473,32 +473,17 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
             U = unit_of(work_of(p, u), u);
             return true;
         }
-        Work w;
-        if (k < p.hyb) {
-            // hybrid decode schedule, phase 1: whole tiles T2 + b + k * grid (one
-            // per CTA per round, never cut), before this CTA's stream-K range
-            const int t = p.T2 + int(blockIdx.x) + k * int(gridDim.x);
-            w.item = w.tile = t;
-            w.tb = 0;
-            w.g0 = 0;
-            w.g1 = p.G;
-            w.S = 1;
-            w.sl = 0;
-            w.cta0 = 0;
-            U = unit_of(w, t);
-            return true;
-        }
-        k -= p.hyb;  // stream-K piece index within this CTA's range
         const uint32_t a = p.skb[blockIdx.x], e = p.skb[blockIdx.x + 1];
         const int it = int(a >> 8) + k, ie = int(e >> 8);
         if (it > ie || (it == ie && (e & 255u) == 0u)) return false;
+        Work w;
         w.item = it;
         w.tb = p.TB == 1 ? 0 : it / p.T;
         w.tile = it - w.tb * p.T;
         w.g0 = k == 0 ? int(a & 255u) : 0;
         w.g1 = it == ie ? int(e & 255u) : p.G;
         w.S = (w.g0 == 0 && w.g1 == p.G) ? 1 : 2;
-        w.sl = k;  // piece index within the range (the decode join's slot choice)
+        w.sl = 0;
         w.cta0 = 0;
         U = unit_of(w, it);
         return true;
@@ -1007,7 +992,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
             if (p.sk) {
                 b_f = sk_cta_of(p, uint32_t(wk.item) << 8);
                 S = sk_cta_of(p, (uint32_t(wk.item) << 8) | uint32_t(p.G - 1)) - b_f + 1;
-                my = 2 * int(blockIdx.x) + (wk.sl == 0 ? 0 : 1);
+                my = 2 * int(blockIdx.x) + (pk == 0 ? 0 : 1);
             }
             if (et == 0) trace_chunk(p, 11, n);
             float4* mine = reinterpret_cast<float4*>(p.part + int64_t(my) * (BN * 128) + r * BN + c0);

@@ -73,8 +73,6 @@ struct GemmParams {
     int32_t dbg;            // development: pipeline-stage bypass bits (MQ_DBG env), 0 in production
     int32_t grid;           // persistent CTAs (<= SMs): CTA b runs units b, b + grid, ...
     const uint8_t* wq;      // merged code+meta blocks (mq_layout.cuh)
-    int32_t hyb;            // hybrid decode schedule: whole-tile rounds before the stream-K range (0: none)
-    int32_t T2;             // hybrid: the stream-K part covers tiles [0, T2), phase 1 tiles [T2, T)
     int64_t n8, n4;         // rows of sub8 / sub4
     const int32_t* colmap;  // [ (T8+T4)*128 ] output column of every tile row
     // EAL activations (tensor-core kernel)

@@ -343,21 +343,3 @@ def test_fast_mode_decode_stream_k(cuda, m, n, k, sched, ag):
         assert np.array_equal(dl.forward(dA, opts=o).cpu().numpy(), Y)
     Yu = dl.forward(dA, opts=mq.exec_opts(capi.MQ_FAST, ag, schedule=1)).cpu().numpy()
     assert _rel(Yu, ref) <= TOL
-
-
-@pytest.mark.parametrize("m,n,k,sched,ag", [(16, 28672, 4096, 3, 128), (16, 28672, 4096, 3, 4096),
-                                            (3, 40000, 1000, 3, 128), (32, 20000, 2048, 3, 128)])
-def test_fast_mode_decode_hybrid(cuda, m, n, k, sched, ag):
-    """Hybrid decode schedule (whole sub4 tiles one per SM, then an equal
-    stream-K share of the rest, cut items joined at the end of a CTA's work):
-    within tolerance and bit-reproducible (opt-in: schedule = 3)."""
-    import torch
-    L, A = _layer(m, n, k, 0.1, seed=53)
-    dl = mq.DeviceLayer(L)
-    dA = torch.from_numpy(A).to(cuda)
-    o = mq.exec_opts(capi.MQ_FAST, ag, schedule=sched)
-    Y = dl.forward(dA, opts=o).cpu().numpy()
-    ref, _, _ = O.mixed_linear(_oracle_layer(L), A, act_group=None if ag == 128 else ag)
-    assert _rel(Y, ref) <= TOL
-    for _ in range(2):
-        assert np.array_equal(dl.forward(dA, opts=o).cpu().numpy(), Y)
