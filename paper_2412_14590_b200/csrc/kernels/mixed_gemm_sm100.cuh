@@ -372,14 +372,16 @@ __device__ __noinline__ void split_join_wide(const GemmParams& p, const Work& wk
     }
 }
 
-// SPL = 1: the wide-tile K-split join is compiled in (launched only for split
-// unit schedules of 64/128-token tiles; its out-of-line call costs the other
-// wide launches ~4% in the accumulation loop's register allocation)
+// SPL = 1: for 64/128-token tiles the wide-tile K-split join is compiled in
+// (launched only for split unit schedules; its out-of-line call costs the other
+// wide launches ~4% in the accumulation loop's register allocation); for decode
+// tiles the stream-K piece decoding (launched only for schedule = 2)
 template <int BN, int MODE, int SPL, int PEER>
 __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mixed_gemm_tc_kernel(const __grid_constant__ GemmParams p) {
     using C = TcCfg<BN>;
     constexpr int NS = C::NS, NE = C::NE, BNE = C::BNE, GPS = C::GPS, NA = C::NA, NT = C::NT, NC = C::NC;
     constexpr bool kSa = (MODE == kExactGroup || MODE == kFastGroup);
+    constexpr bool kSkPath = BN >= 64 || SPL;  // stream-K piece decoding compiled in
     extern __shared__ uint8_t smem_raw[];
     // 1024-B aligned base (SWIZZLE_128B atoms), derived from smem_raw so the
     // compiler keeps shared-space provenance (LDS/STS, not generic LD/ST)
@@ -467,7 +469,10 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
     // of (item, group) positions, cut into one piece per item it touches; a
     // piece that is not a whole item is "split" (S = 2; see sk_piece_done).
     auto piece = [&](int k, Unit& U) -> bool {
-        if (!p.sk) {
+        // decode token tiles compile the stream-K decoding only into their SPL = 1
+        // variant (schedule = 2): every role decodes a piece per unit, and the
+        // extra path costs the default decode launches a few percent
+        if (!(kSkPath && p.sk)) {
             const int u = u0 + k * ustep;
             if (u >= p.units) return false;
             U = unit_of(work_of(p, u), u);
@@ -989,7 +994,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
             // piece uses slot 2b, its last (a head cut at the range end) 2b + 1.
             if constexpr (BN <= 32) {
             int S = wk.S, my = U.key, b_f = wk.cta0;
-            if (p.sk) {
+            if (kSkPath && p.sk) {
                 b_f = sk_cta_of(p, uint32_t(wk.item) << 8);
                 S = sk_cta_of(p, (uint32_t(wk.item) << 8) | uint32_t(p.G - 1)) - b_f + 1;
                 my = 2 * int(blockIdx.x) + (pk == 0 ? 0 : 1);
@@ -1016,9 +1021,9 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
             if (et == 0) trace_chunk(p, 12, n);
             if (last) {
                 // slot of piece j of the item (in order)
-                const bool first_own = p.sk && (p.skb[b_f] >> 8) == uint32_t(wk.item);
+                const bool first_own = kSkPath && p.sk && (p.skb[b_f] >> 8) == uint32_t(wk.item);
                 auto slot_of = [&](int j) -> int64_t {
-                    if (!p.sk) return int64_t(b_f) + j;
+                    if (!(kSkPath && p.sk)) return int64_t(b_f) + j;
                     return int64_t(2 * (b_f + j)) + ((j == 0 && !first_own) ? 1 : 0);
                 };
                 constexpr int V = BNE / 4;      // float4s per piece
@@ -1105,6 +1110,9 @@ cudaError_t launch_bn_mode(const GemmParams& p, bool pdl, cudaStream_t stream) {
     if constexpr (BN >= 64 && (MODE == kFastGroup || MODE == kFastToken)) {
         if (!p.sk && (p.S4 > 1 || p.S8 > 1))
             return launch_kernel<BN, mixed_gemm_tc_kernel<BN, MODE, 1, PEER>>(p, pdl, stream);
+    }
+    if constexpr (BN <= 32 && (MODE == kFastGroup || MODE == kFastToken)) {
+        if (p.sk) return launch_kernel<BN, mixed_gemm_tc_kernel<BN, MODE, 1, PEER>>(p, pdl, stream);  // decode stream-K
     }
     return launch_kernel<BN, mixed_gemm_tc_kernel<BN, MODE, 0, PEER>>(p, pdl, stream);
 }
