@@ -73,6 +73,13 @@ struct TcCfg {
     // (sum a(c - z) = sum a c - z sum a, sum a from K1), so the converter only
     // widens nibbles to bytes and the MMA reads the codes as u8
     static constexpr bool kZpEpi = BN <= 32;
+    // decode: the epilogue reads the activation scales / code sums straight from
+    // the activation stage (released by the epilogue, not the MMA), so the
+    // converter never waits for the activations and runs ahead on the weights
+#ifndef MQ_SA_DIRECT
+#define MQ_SA_DIRECT 1
+#endif
+    static constexpr bool kSaDirect = BN <= 32 && MQ_SA_DIRECT;
     static constexpr int kOffSa = GPS * BN * 128;
     static constexpr int kOffAs = kOffSa + GPS * BN * 4;
     static constexpr int kXStageBytes = ((kOffAs + (kZpEpi ? GPS * BN * 4 : 0)) + 1023) / 1024 * 1024;
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
         }
         for (int s = 0; s < C::NX; ++s) {
             ptx::mbar_init(&xfull[s], 1);
-            ptx::mbar_init(&xempty[s], 1);
+            ptx::mbar_init(&xempty[s], C::kSaDirect ? 4 * NE : 1);
         }
         for (int i = 0; i < NA; ++i) {
             ptx::mbar_init(&afull[i], 4 * NC);
@@ -431,6 +438,14 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
         }
         ptx::mbar_init(tmem_ready, 1);
         ptx::fence_barrier_init();
+    }
+    if constexpr (C::kSaDirect) {
+        // the decode epilogue runs every group of a chunk and reads a short
+        // chunk's unused activation-scale slots (times a zero weight scale):
+        // they must hold finite values before the first copy lands
+        if (warp == 3)
+            for (int i = lane; i < C::NX * GPS * BN; i += 32)
+                reinterpret_cast<float*>(xstage(i / (GPS * BN)) + C::kOffSa)[i % (GPS * BN)] = 0.0f;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -641,7 +656,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                     }
                     ptx::tc_commit(&tfull[rt.idx]);
                     ptx::tc_commit(&aempty[ra.idx]);
-                    ptx::tc_commit(&xempty[rx.idx]);
+                    if (!C::kSaDirect) ptx::tc_commit(&xempty[rx.idx]);
                     if (U.ti.is8) ptx::tc_commit(&empty[rs.idx]);
                 }
                 __syncwarp();
@@ -743,7 +758,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                         }
                     }
                 }
-                if ((kSa || C::kZpEpi) && wg == 0) {
+                if ((kSa || C::kZpEpi) && wg == 0 && !C::kSaDirect) {
                     ptx::mbar_wait(&xfull[rx.idx], rx.ph);
                     if (r < cg * BN) {
                         if (kSa) msw[C::kMetaSa + r] = reinterpret_cast<const float*>(xstage(rx.idx) + C::kOffSa)[r];
@@ -780,7 +795,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
         ptx::tc_fence_after();
         const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_holder);
         griddep_wait();  // scales / output of this launch are ours now
-        Ring rt, rm;
+        Ring rt, rm, rx;
         int n = 0;
         for (int pk = 0;; ++pk) {
             Unit U;
@@ -807,6 +822,12 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                 int gc, cg;
                 chunk_at(U, i, gc, cg);
                 ptx::mbar_wait(&mfull[rm.idx], rm.ph);
+                if constexpr (C::kSaDirect) ptx::mbar_wait(&xfull[rx.idx], rx.ph);  // (complete: the MMA waited it)
+                // activation scales [GPS][BN] (+ code sums): the stage itself, or the meta copy
+                const float* sa_base = C::kSaDirect ? reinterpret_cast<const float*>(xstage(rx.idx) + C::kOffSa)
+                                                    : meta + rm.idx * (C::kMetaSlot / 4) + C::kMetaSa;
+                const int32_t* as_base = C::kSaDirect ? reinterpret_cast<const int32_t*>(xstage(rx.idx) + C::kOffAs)
+                                                      : reinterpret_cast<const int32_t*>(meta + rm.idx * (C::kMetaSlot / 4)) + C::kMetaAs;
                 ptx::mbar_wait(&tfull[rt.idx], rt.ph);
                 ptx::tc_fence_after();
                 if (n == 0 && et == 0) trace(p, 3);
@@ -832,10 +853,10 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                             const int j = j0 + h;
                             const float sw = msw[j * 128 + r];
                             const float2 sw2 = pk2(sw, sw);
-                            const float* sav = msw + C::kMetaSa + j * BN + c0;
+                            const float* sav = sa_base + j * BN + c0;
                             if constexpr (C::kZpEpi) {  // S = sum a c - z sum a (exact int32)
                                 const int32_t zr = reinterpret_cast<const int32_t*>(msw)[C::kMetaZp + j * 128 + r];
-                                const int32_t* asv = reinterpret_cast<const int32_t*>(msw) + C::kMetaAs + j * BN + c0;
+                                const int32_t* asv = as_base + j * BN + c0;
 #pragma unroll
                                 for (int q = 0; q < BNE; ++q) v[h][q] = uint32_t(int32_t(v[h][q]) + zr * asv[q]);  // zr = -z
                             }
@@ -852,7 +873,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                 } else
                 for (int j = 0; j < cg; ++j) {
                     const float sw = msw[j * 128 + r];
-                    const float* sav = msw + C::kMetaSa + j * BN + c0;
+                    const float* sav = sa_base + j * BN + c0;
                     const float2 sw2 = pk2(sw, sw);
                     const uint32_t tcol = uint32_t((rt.idx * GPS + j) * BN + c0);
 #ifndef MQ_CW64
@@ -877,7 +898,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                         ptx::tmem_wait_ld();
                         if constexpr (C::kZpEpi) {  // S = sum a c - z sum a (exact int32)
                             const int32_t zr = reinterpret_cast<const int32_t*>(msw)[C::kMetaZp + j * 128 + r];
-                            const int32_t* asv = reinterpret_cast<const int32_t*>(msw) + C::kMetaAs + j * BN + c0 + ch * CW;
+                            const int32_t* asv = as_base + j * BN + c0 + ch * CW;
 #pragma unroll
                             for (int q = 0; q < CW; ++q) v[q] = uint32_t(int32_t(v[q]) + zr * asv[q]);  // zr = -z
                         }
@@ -932,10 +953,12 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                 if (lane == 0) {
                     ptx::mbar_arrive(&tempty[rt.idx]);
                     ptx::mbar_arrive(&mempty[rm.idx]);
+                    if constexpr (C::kSaDirect) ptx::mbar_arrive(&xempty[rx.idx]);
                 }
                 if (et == 0) trace_chunk(p, 4, n);
                 rt.next<NT>();
                 rm.next<C::NM>();
+                rx.next<C::NX>();
             }
             if (et == 0) trace(p, 4);
             if constexpr (kPair) {
