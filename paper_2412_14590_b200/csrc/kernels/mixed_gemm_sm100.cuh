@@ -89,11 +89,12 @@ struct TcCfg {
 #define MQ_NX16 8
 #endif
 #ifndef MQ_NX32
-#define MQ_NX32 3
+#define MQ_NX32 4
 #endif
     // (16-token tiles: 8 activation stages and 3 weight stages beat 3 + 5 — the
     // activations come from L2 under full HBM streaming, so their ring needs the
-    // depth; M <= 16 stack -2%. 32-token tiles: 3 — 6 was 9% slower)
+    // depth; M <= 16 stack -2%. 32-token tiles, 4-group chunks: 4 — 3 and 5 were
+    // 8% slower)
     static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? 6 : BN == 16 ? MQ_NX16 : MQ_NX32;
     // TMEM rings: NT accumulator chunk slots of GPS x BN int32 columns, NA
     // A-operand chunk slots of GPS x 32 columns (128 int8 K per row).

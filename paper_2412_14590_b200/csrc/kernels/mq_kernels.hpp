@@ -138,9 +138,15 @@ cudaError_t launch_mixed_gemm_tc(const GemmParams& p, int token_tile, int mode, 
 #ifndef MQ_GPS_SMALL
 #define MQ_GPS_SMALL 4
 #endif
-// (A/B in graph: 16-token tiles stream best with 4-group chunks; from 32 tokens
-// the per-chunk rescale is longer and 2-group chunks pipeline better)
-constexpr int gemm_gps(int token_tile) { return token_tile <= 16 ? MQ_GPS_SMALL : (token_tile <= 64 ? 2 : 1); }
+// (A/B in graph: 16- and 32-token tiles stream best with 4-group chunks — at
+// decode the per-chunk hand-offs dominate; M = 24-32 stack -3..5% vs 2-group
+// chunks with 4 activation stages; 64-token tiles 2, 128-token tiles 1 (TMEM))
+#ifndef MQ_GPS32
+#define MQ_GPS32 4
+#endif
+constexpr int gemm_gps(int token_tile) {
+    return token_tile <= 16 ? MQ_GPS_SMALL : token_tile <= 32 ? MQ_GPS32 : (token_tile <= 64 ? 2 : 1);
+}
 int gemm_stages(int token_tile);
 // SIMT debug kernel (same weight layout, exact op order, row-major activations).
 cudaError_t launch_mixed_gemm_simt(const GemmParams& p, const int8_t* codes, int64_t ldc,
