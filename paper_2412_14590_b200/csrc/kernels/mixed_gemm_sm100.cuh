@@ -95,7 +95,10 @@ struct TcCfg {
     // activations come from L2 under full HBM streaming, so their ring needs the
     // depth; M <= 16 stack -2%. 32-token tiles, 4-group chunks: 4 — 3 and 5 were
     // 8% slower)
-    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? 6 : BN == 16 ? MQ_NX16 : MQ_NX32;
+#ifndef MQ_NX64
+#define MQ_NX64 6
+#endif
+    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? MQ_NX64 : BN == 16 ? MQ_NX16 : MQ_NX32;
     // TMEM rings: NT accumulator chunk slots of GPS x BN int32 columns, NA
     // A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
