@@ -40,6 +40,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "mq_kernels.hpp"
 #include "mq_ptx.cuh"
 
@@ -98,7 +100,10 @@ struct TcCfg {
 #ifndef MQ_NX64
 #define MQ_NX64 6
 #endif
-    static constexpr int NX = BN >= 128 ? 8 : BN >= 64 ? MQ_NX64 : BN == 16 ? MQ_NX16 : MQ_NX32;
+#ifndef MQ_NX128
+#define MQ_NX128 8
+#endif
+    static constexpr int NX = BN >= 128 ? MQ_NX128 : BN >= 64 ? MQ_NX64 : BN == 16 ? MQ_NX16 : MQ_NX32;
     // TMEM rings: NT accumulator chunk slots of GPS x BN int32 columns, NA
     // A-operand chunk slots of GPS x 32 columns (128 int8 K per row).
     static constexpr uint32_t kAccPerChunk = GPS * BN, kAPerChunk = GPS * 32;
@@ -183,20 +188,48 @@ __device__ __forceinline__ void trace_chunk(const GemmParams& p, int ev, int n) 
         p.trace[148 * 8 + ev * 64 + n] = clock64();
 }
 
-__device__ __forceinline__ void store_one(void* Y, int dt, int64_t idx, float v) {
-    if (dt == 0) static_cast<float*>(Y)[idx] = v;
-    else if (dt == 1) static_cast<__half*>(Y)[idx] = __float2half_rn(v);
-    else static_cast<__nv_bfloat16*>(Y)[idx] = __float2bfloat16_rn(v);
+// One thread's output row: tokens m0 .. m0 + BNE - 1 of original column col
+// (col < 0: a padding row), the dtype switch and the bounds hoisted out of the
+// per-token loop, the address advanced by one row stride per token (a
+// per-element dtype switch and 64-bit index made the scatter ~20% of a prefill
+// launch). The PEER kernel variant (the fused gather, mq_mixed_linear_peers,
+// npeer > 1) also stores every element into each peer rank's copy of Y at the
+// same (original) column, over NVLink — a separate instantiation
+// (mixed_gemm_peers.cu): the peer loop costs the plain kernels ~20% at prefill.
+template <typename T>
+__device__ __forceinline__ T to_out(float v) {
+    if constexpr (std::is_same<T, __half>::value) return __float2half_rn(v);
+    else if constexpr (std::is_same<T, __nv_bfloat16>::value) return __float2bfloat16_rn(v);
+    else return v;
 }
-// The output element at idx; the PEER kernel variant (the fused gather,
-// mq_mixed_linear_peers, npeer > 1) also stores it into every peer rank's copy
-// of Y at the same (original) column, over NVLink. A separate instantiation
-// (mixed_gemm_peers.cu): the loop costs the plain kernels ~20% at prefill.
-template <int PEER>
-__device__ __forceinline__ void store_out(const GemmParams& p, int64_t idx, float v) {
-    store_one(p.Y, p.out_dtype, idx, v);
+template <typename T, int BNE, int MODE>
+__device__ __forceinline__ void store_col(void* Y, int64_t ldy, int64_t m0, int col, int jn, const float* v,
+                                          const float* sa) {
+    T* y = static_cast<T*>(Y) + (m0 * ldy + col);
+#pragma unroll
+    for (int j = 0; j < BNE; ++j) {
+        if (j < jn) {
+            float x = v[j];
+            if constexpr (MODE == kFastToken) x = __fmul_rn(x, __ldg(sa + m0 + j));
+            *y = to_out<T>(x);
+        }
+        y += ldy;
+    }
+}
+template <typename T, int BNE, int MODE, int PEER>
+__device__ __forceinline__ void store_cols(const GemmParams& p, int64_t m0, int col, int jn, const float* v) {
+    store_col<T, BNE, MODE>(p.Y, p.ldy, m0, col, jn, v, p.sa);
     if constexpr (PEER)
-        for (int i = 1; i < p.npeer; ++i) store_one(p.ypeer[i], p.out_dtype, idx, v);
+        for (int i = 1; i < p.npeer; ++i) store_col<T, BNE, MODE>(p.ypeer[i], p.ldy, m0, col, jn, v, p.sa);
+}
+template <int BNE, int MODE, int PEER>
+__device__ __forceinline__ void store_tokens(const GemmParams& p, int64_t m0, int col, const float* v) {
+    if (col < 0) return;
+    const int64_t rem = p.M - m0;
+    const int jn = rem < BNE ? int(rem) : BNE;
+    if (p.out_dtype == 1) store_cols<__half, BNE, MODE, PEER>(p, m0, col, jn, v);
+    else if (p.out_dtype == 2) store_cols<__nv_bfloat16, BNE, MODE, PEER>(p, m0, col, jn, v);
+    else store_cols<float, BNE, MODE, PEER>(p, m0, col, jn, v);
 }
 
 // ring position: slot index + phase parity
@@ -369,17 +402,8 @@ __device__ __noinline__ void split_join_wide(const GemmParams& p, const Work& wk
             sum.z = __fadd_rn(sum.z, t.z);
             sum.w = __fadd_rn(sum.w, t.w);
         }
-        if (col < 0) continue;
         const float v4[4] = {sum.x, sum.y, sum.z, sum.w};
-#pragma unroll
-        for (int e4 = 0; e4 < 4; ++e4) {
-            const int64_t m = m0 + j + e4;
-            if (m < p.M) {
-                float v = v4[e4];
-                if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                store_out<PEER>(p, m * p.ldy + col, v);
-            }
-        }
+        store_tokens<4, MODE, PEER>(p, m0 + j, col, v4);
     }
 }
 
@@ -975,19 +999,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
             if (MODE == kDumpPartials || U.nch == 0) continue;
             // scatter this thread's row to its original output column
             const int col = (r < ti.rows && !(dbg_bits(p) & 128)) ? __ldg(p.colmap + wk.tile * kTileRows + r) : -1;
-            auto store_acc = [&]() {
-                if (col >= 0) {
-#pragma unroll
-                    for (int j = 0; j < BNE; ++j) {
-                        const int64_t m = m0 + j;
-                        if (m < p.M) {
-                            float v = acc[j];
-                            if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                            store_out<PEER>(p, m * p.ldy + col, v);
-                        }
-                    }
-                }
-            };
+            auto store_acc = [&]() { store_tokens<BNE, MODE, PEER>(p, m0, col, acc); };
             if (wk.S == 1) {  // whole-K tile
                 if (et == 0) trace_chunk(p, 11, n);
                 store_acc();
@@ -1078,17 +1090,7 @@ __global__ void __launch_bounds__(TcCfg<BN>::kThreads, TcCfg<BN>::kMinBlocks) mi
                     }
                 }
                 if (et == 0) trace_chunk(p, 15, 8);
-                if (col >= 0) {
-#pragma unroll
-                    for (int j = 0; j < BNE; ++j) {
-                        const int64_t m = m0 + j;
-                        if (m < p.M) {
-                            float v = sum[j];
-                            if constexpr (MODE == kFastToken) v = __fmul_rn(v, __ldg(p.sa + m));
-                            store_out<PEER>(p, m * p.ldy + col, v);
-                        }
-                    }
-                }
+                store_tokens<BNE, MODE, PEER>(p, m0, col, sum);
             }
             }  // BN <= 32
         }

@@ -10,7 +10,7 @@ from paper_2412_14590_b200 import capi
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 SH = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)]
 for (N, K) in SH:
-    W, A, prom = mq.bench_inputs(M, N, K, 0.1, 1)
+    W, A, prom = mq.bench_inputs(M, N, K, float(os.environ.get("FRAC", "0.1")), 1)
     L = mq.partition_and_quantize(W, prom)
     reps = [mq.DeviceLayer(L) for _ in range(2)]
     dA = torch.from_numpy(A).cuda()
@@ -35,4 +35,4 @@ for (N, K) in SH:
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / 200
     wb = reps[0].info.weight_stream_bytes
-    print(f"sched={os.environ.get('SCHED', '0')} ks={os.environ.get('KSPLIT', '0')} dbg={os.environ.get('MQ_DBG', '0'):>3s} N={N} K={K} M={M}: {us:6.2f} us/launch  {wb / us / 1e3:6.0f} GB/s", flush=True)
+    print(f"sched={os.environ.get('SCHED', '0')} ks={os.environ.get('KSPLIT', '0')} dbg={os.environ.get('MQ_DBG', '0'):>3s} frac={os.environ.get('FRAC', '0.1')} N={N} K={K} M={M}: {us:6.2f} us/launch  {wb / us / 1e3:6.0f} GB/s", flush=True)
