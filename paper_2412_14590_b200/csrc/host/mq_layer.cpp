@@ -85,13 +85,27 @@ struct Plan {
 // launches when the unit schedule's last round would leave CTAs idle for
 // longer than a cut item costs; every CTA range covers at least one item's
 // length, so an item is cut at most once (head + tail, sk_piece_done).
+// Prefill stream-K: a sub8 item's extra cost, in sub4 groups — its epilogue
+// scatters to the sparse salient columns (~20 sectors per warp store instead
+// of 2). Measured on the Llama-8B shapes at M = 512: 4 balances gate_up
+// (142 -> 132 us); 8 pushes qkv below stream_k_pays' cover bound.
+int sk_extra8() {
+    static const int e = [] {
+        const char* v = std::getenv("MQ_SK_E8");  // development override
+        return v ? std::atoi(v) : 4;
+    }();
+    return e;
+}
+
 bool stream_k_pays(const mq_layer_s* L, const Plan* pl, bool force) {
     const int64_t G = L->G, items = int64_t(pl->tb) * (L->tiles8 + L->tiles4);
     const int grid = std::min<int>(L->num_sms, kSkMax);
-    const double per_cta = double(items * G) / grid;  // groups (prefill: a sub8 group costs as a sub4 one)
+    const int64_t E = sk_extra8();
+    // groups per CTA (a sub8 item costs G + E sub4 groups: its scattered stores)
+    const double per_cta = double(pl->tb * (L->tiles8 * (G + E) + L->tiles4 * G)) / grid;
     // every CTA range (less the chunk rounding of its ends) must cover a whole
     // item's length, so no item is cut twice (head + tail, sk_piece_done)
-    if (per_cta < double(G + 2 * gemm_gps(pl->bn) + 1)) return false;
+    if (per_cta * double(G) / double(G + E) < double(G + 2 * gemm_gps(pl->bn) + 1)) return false;
     if (force) return true;
     const int64_t rounds = (items + grid - 1) / grid;
     // measured (BN = 64 and 128): publish + join + tail of a cut item ~ 16 groups
@@ -110,9 +124,11 @@ bool decode_stream_k_pays(const mq_layer_s*, bool force) { return force; }
 
 void plan_stream_k(const mq_layer_s* L, Plan* pl) {
     const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4, T = T8 + T4;
-    const int64_t c8 = pl->bn <= 32 ? 2 : 1;
+    // cost of a sub8 / sub4 group: decode streams twice the bytes for a sub8
+    // group; prefill spreads a sub8 item's extra cost E over its G groups
+    const int64_t c8 = pl->bn <= 32 ? 2 : G + sk_extra8(), c4 = pl->bn <= 32 ? 1 : G;
     const int gps = gemm_gps(pl->bn), gps8 = gps / 2 > 0 ? gps / 2 : 1;
-    const int64_t ctb = T8 * G * c8 + T4 * G, total = ctb * pl->tb;
+    const int64_t ctb = T8 * G * c8 + T4 * G * c4, total = ctb * pl->tb;
     const int64_t chunks = (T8 * ((G + gps8 - 1) / gps8) + T4 * ((G + gps - 1) / gps)) * pl->tb;
     const int grid = static_cast<int>(std::min<int64_t>({L->num_sms, kSkMax, chunks}));
     pl->skb.assign(size_t(grid) + 1, 0);
@@ -126,8 +142,8 @@ void plan_stream_k(const mq_layer_s* L, Plan* pl) {
             g = g / gps8 * gps8;
         } else {
             const int64_t r4 = rr - T8 * G * c8;
-            t = T8 + r4 / G;
-            g = r4 - (t - T8) * G;
+            t = T8 + r4 / (G * c4);
+            g = (r4 - (t - T8) * G * c4) / c4;
             g = g / gps * gps;
         }
         pl->skb[b] = static_cast<uint32_t>(((tb * T + t) << 8) | g);
