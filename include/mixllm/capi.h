@@ -243,7 +243,8 @@ typedef enum { MQ_EXACT = 0, MQ_FAST = 1 } mq_mode;
 typedef struct {
     int32_t mode;        /* mq_mode */
     int32_t act_group;   /* group size the activation scales use (g or K) */
-    int32_t ksplit;      /* MQ_FAST: 0 = auto, 1 = no K splitting, 2..8 = K-slices per sub4 tile */
+    int32_t ksplit;      /* MQ_FAST: 0 = auto, 1 = no K splitting, 2..8 = K-slices per sub4 tile (64/128-token
+                            tiles: reduced until every slice runs in one round of the grid) */
     int32_t token_tile;  /* 0 = auto; else 16/32/64/128 */
     int32_t gemm_impl;   /* 0 = tcgen05 (product); 1 = SIMT debug kernel */
     int32_t no_pdl;      /* 1 = plain launches (default: programmatic dependent launch) */

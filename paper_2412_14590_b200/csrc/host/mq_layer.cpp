@@ -171,6 +171,10 @@ void plan_stream_k(const mq_layer_s* L, Plan* pl) {
 // rescale work and a split join moves a 32 / 64 KB partial
 void best_split(mq_layer_s* L, int kind) {
     const double kUnitCost = 2.0, kSplitCost = kind == 0 ? 4.0 : kind == 1 ? 8.0 : 16.0, k8 = kind == 0 ? 2.0 : 1.0;
+    // (charging sub8 items their scatter cost here, sk_extra8, moves the
+    // 64-token launches' plans to S8 = 2 S4: 2.3 us faster over the four
+    // projections launched alone, no faster inside the PDL-chained stack)
+    const double e8 = 0.0;
     const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4;
     double best = 1e30;
     for (int S4 = 1; S4 <= 8; S4 *= 2) {
@@ -178,7 +182,9 @@ void best_split(mq_layer_s* L, int kind) {
             if (S4 > G || S8 > G) continue;
             const int64_t u8 = T8 * S8, units = u8 + T4 * S4;
             const int64_t grid = std::min<int64_t>(units, L->num_sms);
-            const double c8 = k8 * double(G) / S8 + kUnitCost + (S8 > 1 ? kSplitCost : 0.0);
+            // wide tiles: split items only when every slice runs in one round (the together-mode join)
+            if (kind > 0 && S8 > 1 && units > L->num_sms) continue;
+            const double c8 = (k8 * double(G) + e8) / S8 + kUnitCost + (S8 > 1 ? kSplitCost : 0.0);
             const double c4 = double(G) / S4 + kUnitCost + (S4 > 1 ? kSplitCost : 0.0);
             double span = 0;
             for (int64_t b = 0; b < grid; ++b) {  // CTA b runs units b, b + grid, ...
@@ -234,6 +240,14 @@ void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
         pl->S4 = best;
         pl->S8 = 2 * best;
         while (pl->S8 > 1 && pl->S8 > L->G) pl->S8 >>= 1;
+        // wide token tiles: the slices of an item must run in one round (the
+        // together-mode join); a multi-round split of 64/128-token tiles joins
+        // through one CTA per tile and measured 3-20x slower
+        while (pl->bn > 32 && (pl->S4 > 1 || pl->S8 > 1) &&
+               (int64_t(pl->S8) * L->tiles8 + int64_t(pl->S4) * L->tiles4) * pl->tb > L->num_sms) {
+            pl->S4 = std::max(pl->S4 >> 1, 1);
+            pl->S8 = std::max(pl->S8 >> 1, 1);
+        }
         return;
     }
     const int kind = pl->bn <= 32 ? 0 : pl->bn == 64 ? 1 : 2;  // best_split, computed once per layer
