@@ -269,3 +269,48 @@ def step_d2h(r, which):
 
 for w in ((), (3,), (0,), (0, 1, 2), (0, 1, 2, 3)):
     print(f"D2H of outputs {w}: {tg(graphs(lambda r, w=w: step_d2h(r, w))):.1f} us")
+
+
+def step_out(r, zc_out=(0, 1, 2, 3), h2d=True):
+    """bench-style inputs (layer 0 zero-copy, the others by copy engine, or all
+    device-resident when h2d is False); the outputs of the layers in zc_out are
+    written by K2's epilogue straight into pinned host memory (no copy), the
+    others by copy engine (the last one by a copy kernel)."""
+    main = torch.cuda.current_stream()
+    fork = torch.cuda.Event()
+    fork.record(main)
+    s_in.wait_event(fork)
+    s_out.wait_event(fork)
+    ready = [None] * 4
+    if h2d:
+        with torch.cuda.stream(s_in):
+            for i in range(1, 4):
+                dxs[i].copy_(hxs[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_in)
+                ready[i] = ev
+    for i in range(4):
+        if ready[i] is not None:
+            main.wait_event(ready[i])
+        x = hxv[0] if (i == 0 and h2d) else xv[i]
+        if i in zc_out:
+            layers[i][r].forward(x, out=hyv[i], opts=opts)
+            continue
+        layers[i][r].forward(x, out=yv[i], opts=opts)
+        if i == 3:
+            torch.add(yv[i], 0, out=hyv[i])
+            continue
+        done = torch.cuda.Event()
+        done.record(main)
+        s_out.wait_event(done)
+        with torch.cuda.stream(s_out):
+            hys[i].copy_(dys[i], non_blocking=True)
+    for st in (s_out, s_in):
+        j = torch.cuda.Event()
+        j.record(st)
+        main.wait_event(j)
+
+
+for w in ((), (3,), (2, 3), (0, 1, 2, 3)):
+    print(f"epilogue-to-host outputs {w}: e2e {tg(graphs(lambda r, w=w: step_out(r, w))):.1f} us, "
+          f"device inputs {tg(graphs(lambda r, w=w: step_out(r, w, h2d=False))):.1f} us")
