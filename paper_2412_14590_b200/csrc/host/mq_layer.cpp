@@ -64,10 +64,24 @@ mq_status cuda_fail(cudaError_t e, const char* what) {
         if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
     } while (0)
 
-int auto_token_tile(int64_t M) {
+// 128-token tiles past M = 64, except on a narrow layer with short K, where
+// 128-token items would leave most SMs idle and K is too short to split
+// (qkv 6144x4096 at M = 128: 49 items; 64-token tiles, 98 items: 23.7 -> 18.2
+// us; o 4096x4096: 20.7 -> 17.6 us; the batch-192 stack's qkv and o: -25%).
+// Long-K layers split K instead (down 4096x14336 stays at 128: 32.2 vs 33.8 us).
+#ifndef MQ_TT64_MAX
+#define MQ_TT64_MAX 256
+#endif
+int auto_token_tile(const mq_layer_s* L, int64_t M) {
     if (M <= 16) return 16;
     if (M <= 32) return 32;
     if (M <= 64) return 64;
+    static const int rule = [] {
+        const char* v = std::getenv("MQ_TT_RULE");  // development A/B
+        return v ? std::atoi(v) : 1;
+    }();
+    const int64_t items128 = (M + 127) / 128 * (L->tiles8 + L->tiles4);
+    if (rule && items128 < L->num_sms && L->G <= 64 && M <= int64_t(MQ_TT64_MAX)) return 64;
     return 128;
 }
 
@@ -277,7 +291,7 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     pl->pf_bytes = o->prefetch_bytes;
     if (pl->pf_bytes < 0) return fail(MQ_USAGE, "prefetch_bytes must be >= 0");
     if (o->ksplit < 0 || o->ksplit > 8) return fail(MQ_USAGE, "ksplit must be 0 (auto), 1 (none) or a split <= 8");
-    pl->bn = o->token_tile ? o->token_tile : auto_token_tile(M);
+    pl->bn = o->token_tile ? o->token_tile : auto_token_tile(L, M);
     if (pl->bn != 16 && pl->bn != 32 && pl->bn != 64 && pl->bn != 128)
         return fail(MQ_USAGE, "token_tile must be 16, 32, 64 or 128");
     pl->tb = static_cast<int>((M + pl->bn - 1) / pl->bn);
