@@ -302,7 +302,12 @@ size_t mq_mixed_linear_workspace_bytes(mq_layer_t layer, int64_t M, const mq_exe
  * any of those layers, run K2 on it. The EAL sits at an offset that depends
  * only on (K, M, options); each layer's split-K partials follow it, so the
  * workspace must be >= the MAXIMUM of mq_mixed_linear_workspace_bytes over the
- * layers that share it. Same results as mq_mixed_linear. */
+ * layers that share it. The token tile depends on M only here (the EAL is
+ * shared); the fused mq_mixed_linear may pick a per-layer tile for a narrow,
+ * short-K layer. Same results as mq_mixed_linear: bit-identical in MQ_EXACT
+ * mode and whenever opts.token_tile is set; otherwise, in MQ_FAST mode, equal
+ * within its rounding (a different tile changes the K-split and summation
+ * order). */
 mq_status mq_quantize_act_ws(mq_layer_t layer, const void* A, mq_dtype a_dtype, int64_t M,
                              const mq_exec_opts* opts, void* workspace, int32_t* err, void* stream);
 mq_status mq_mixed_linear_ws(mq_layer_t layer, int64_t M, const void* workspace, void* Y,

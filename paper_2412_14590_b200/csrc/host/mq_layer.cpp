@@ -64,25 +64,34 @@ mq_status cuda_fail(cudaError_t e, const char* what) {
         if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
     } while (0)
 
-// 128-token tiles past M = 64, except on a narrow layer with short K, where
-// 128-token items would leave most SMs idle and K is too short to split
-// (qkv 6144x4096 at M = 128: 49 items; 64-token tiles, 98 items: 23.7 -> 18.2
-// us; o 4096x4096: 20.7 -> 17.6 us; the batch-192 stack's qkv and o: -25%).
-// Long-K layers split K instead (down 4096x14336 stays at 128: 32.2 vs 33.8 us).
+// Token tile per launch: 16 / 32 / 64 / 128 by M, except on a narrow, short-K
+// layer (G <= 64, where K-splitting has little to split), which takes the
+// smallest tile whose token blocks x tiles still fit one round of the SMs:
+// more, smaller items instead of idle SMs (graph-timed launches, Llama-8B):
+// qkv 6144x4096 at M = 48: 64 -> 16-token tiles (147 items) 17.0 -> 12.4 us;
+// at M = 80-96: 32-token tiles 18.1 -> 15.9 us; o 4096x4096 at M = 64: 16-token
+// tiles 13.7 -> 12.4 us, at M = 128: 32-token tiles 17.6 -> 15.8 us. When no
+// tile fits one round, 64-token tiles while the 128-token items leave SMs idle
+// (qkv at M = 128: 23.7 -> 18.2 us). Long-K layers split K instead (down
+// 4096x14336 keeps its tile).
 #ifndef MQ_TT64_MAX
 #define MQ_TT64_MAX 256
 #endif
-int auto_token_tile(const mq_layer_s* L, int64_t M) {
+int auto_token_tile(const mq_layer_s* L, int64_t M, bool per_layer) {
     if (M <= 16) return 16;
     if (M <= 32) return 32;
-    if (M <= 64) return 64;
     static const int rule = [] {
-        const char* v = std::getenv("MQ_TT_RULE");  // development A/B
-        return v ? std::atoi(v) : 1;
+        const char* v = std::getenv("MQ_TT_RULE");  // development A/B: 0 off, 1 64-only, 2 full
+        return v ? std::atoi(v) : 2;
     }();
-    const int64_t items128 = (M + 127) / 128 * (L->tiles8 + L->tiles4);
-    if (rule && items128 < L->num_sms && L->G <= 64 && M <= int64_t(MQ_TT64_MAX)) return 64;
-    return 128;
+    const int64_t T = L->tiles8 + L->tiles4;
+    if (per_layer && rule && L->G <= 64 && M <= int64_t(MQ_TT64_MAX)) {
+        if (rule >= 2)
+            for (int bn = 16; bn <= 64; bn *= 2)
+                if ((M + bn - 1) / bn * T <= L->num_sms) return bn;
+        if (M > 64 && (M + 127) / 128 * T < L->num_sms) return 64;
+    }
+    return M <= 64 ? 64 : 128;
 }
 
 struct Plan {
@@ -269,7 +278,10 @@ void choose_split(const mq_layer_s* L, Plan* pl, int ksplit) {
     pl->S8 = L->split8[kind];
 }
 
-mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl) {
+// shared_acts: the split API (mq_quantize_act_ws + mq_mixed_linear_ws), where one
+// quantized activation feeds several layers, so the token tile (hence the EAL
+// layout) must depend on M only, not on the layer
+mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan* pl, bool shared_acts = false) {
     mq_exec_opts d{};
     if (!o) o = &d;
     const int act_group = o->act_group ? o->act_group : L->group;
@@ -291,7 +303,7 @@ mq_status make_plan(const mq_layer_s* L, int64_t M, const mq_exec_opts* o, Plan*
     pl->pf_bytes = o->prefetch_bytes;
     if (pl->pf_bytes < 0) return fail(MQ_USAGE, "prefetch_bytes must be >= 0");
     if (o->ksplit < 0 || o->ksplit > 8) return fail(MQ_USAGE, "ksplit must be 0 (auto), 1 (none) or a split <= 8");
-    pl->bn = o->token_tile ? o->token_tile : auto_token_tile(L, M);
+    pl->bn = o->token_tile ? o->token_tile : auto_token_tile(L, M, !shared_acts);
     if (pl->bn != 16 && pl->bn != 32 && pl->bn != 64 && pl->bn != 128)
         return fail(MQ_USAGE, "token_tile must be 16, 32, 64 or 128");
     pl->tb = static_cast<int>((M + pl->bn - 1) / pl->bn);
@@ -806,9 +818,9 @@ mq_status mq_quantize_act_scheme(const void* A, mq_dtype dt, int64_t M, int64_t 
 }
 
 size_t mq_forward_workspace_bytes(mq_layer_t L, int64_t M, const mq_exec_opts* o) {
-    Plan pl;
-    if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK) return 0;
-    return eal_ws_layout(L, pl).total;
+    Plan pl, ps;  // a workspace serves the fused forward and the split API
+    if (!L || M <= 0 || make_plan(L, M, o, &pl) != MQ_OK || make_plan(L, M, o, &ps, true) != MQ_OK) return 0;
+    return std::max(eal_ws_layout(L, pl).total, eal_ws_layout(L, ps).total);
 }
 
 namespace {
@@ -907,7 +919,7 @@ mq_status mq_quantize_act_ws(mq_layer_t L, const void* A, mq_dtype a_dtype, int6
     if (M == 0) return MQ_OK;
     if (a_dtype != MQ_F32 && a_dtype != MQ_F16 && a_dtype != MQ_BF16) return fail(MQ_USAGE, "bad activation dtype");
     Plan pl;
-    if (mq_status st = make_plan(L, M, o, &pl)) return st;
+    if (mq_status st = make_plan(L, M, o, &pl, true)) return st;
     const EalWs w = eal_ws_layout(L, pl);
     uint8_t* base = static_cast<uint8_t*>(ws);
     cudaError_t e = launch_act_quant_eal(A, a_dtype, M, L->K, L->K, pl.per_token ? int(L->K) : L->group, pl.Mpad,
@@ -925,7 +937,7 @@ mq_status mq_mixed_linear_ws(mq_layer_t L, int64_t M, const void* ws, void* Y, m
     if (M == 0) return MQ_OK;
     if (out_dtype != MQ_F32 && out_dtype != MQ_F16 && out_dtype != MQ_BF16) return fail(MQ_USAGE, "bad output dtype");
     Plan pl;
-    if (mq_status st = make_plan(L, M, o, &pl)) return st;
+    if (mq_status st = make_plan(L, M, o, &pl, true)) return st;
     return launch_k2(L, pl, ws, M, Y, out_dtype, static_cast<cudaStream_t>(stream));
 }
 
