@@ -70,9 +70,8 @@ mq_status cuda_fail(cudaError_t e, const char* what) {
 // more, smaller items instead of idle SMs (graph-timed launches, Llama-8B):
 // qkv 6144x4096 at M = 48: 64 -> 16-token tiles (147 items) 17.0 -> 12.4 us;
 // at M = 80-96: 32-token tiles 18.1 -> 15.9 us; o 4096x4096 at M = 64: 16-token
-// tiles 13.7 -> 12.4 us, at M = 128: 32-token tiles 17.6 -> 15.8 us. When no
-// tile fits one round, 64-token tiles while the 128-token items leave SMs idle
-// (qkv at M = 128: 23.7 -> 18.2 us). Long-K layers split K instead (down
+// tiles 13.7 -> 12.4 us, at M = 128: 32-token tiles 17.6 -> 15.8 us; qkv at
+// M = 128: 64-token tiles 23.7 -> 18.2 us. Long-K layers split K instead (down
 // 4096x14336 keeps its tile).
 #ifndef MQ_TT64_MAX
 #define MQ_TT64_MAX 256
@@ -81,16 +80,13 @@ int auto_token_tile(const mq_layer_s* L, int64_t M, bool per_layer) {
     if (M <= 16) return 16;
     if (M <= 32) return 32;
     static const int rule = [] {
-        const char* v = std::getenv("MQ_TT_RULE");  // development A/B: 0 off, 1 64-only, 2 full
+        const char* v = std::getenv("MQ_TT_RULE");  // development A/B: 0 off, 1 64 only, 2 all
         return v ? std::atoi(v) : 2;
     }();
     const int64_t T = L->tiles8 + L->tiles4;
-    if (per_layer && rule && L->G <= 64 && M <= int64_t(MQ_TT64_MAX)) {
-        if (rule >= 2)
-            for (int bn = 16; bn <= 64; bn *= 2)
-                if ((M + bn - 1) / bn * T <= L->num_sms) return bn;
-        if (M > 64 && (M + 127) / 128 * T < L->num_sms) return 64;
-    }
+    if (per_layer && rule && L->G <= 64 && M <= int64_t(MQ_TT64_MAX))
+        for (int bn = rule >= 2 ? 16 : 64; bn <= 64; bn *= 2)
+            if ((M + bn - 1) / bn * T <= L->num_sms) return bn;
     return M <= 64 ? 64 : 128;
 }
 
