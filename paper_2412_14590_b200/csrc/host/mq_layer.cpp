@@ -233,6 +233,7 @@ void best_split_blocks(const mq_layer_s* L, int kind, int tb, int* S4o, int* S8o
         if (S > G) break;
         const int64_t per_tb = (T8 + T4) * S, units = per_tb * tb;
         const int64_t grid = std::min<int64_t>(units, L->num_sms);
+        if (S > 1 && units > L->num_sms) break;  // split items only within one round (see choose_split)
         std::fill(cta.begin(), cta.end(), 0.0);
         const double c = double(G) / S + kUnitCost + (S > 1 ? kSplitCost : 0.0);
         for (int64_t u = 0; u < units; ++u) cta[size_t(u % grid)] += c;
