@@ -190,10 +190,9 @@ void plan_stream_k(const mq_layer_s* L, Plan* pl) {
 // rescale work and a split join moves a 32 / 64 KB partial
 void best_split(mq_layer_s* L, int kind) {
     const double kUnitCost = 2.0, kSplitCost = kind == 0 ? 4.0 : kind == 1 ? 8.0 : 16.0, k8 = kind == 0 ? 2.0 : 1.0;
-    // (charging sub8 items their scatter cost here, sk_extra8, moves the
+    // (charging sub8 items their scatter cost here too, sk_extra8, moves the
     // 64-token launches' plans to S8 = 2 S4: 2.3 us faster over the four
     // projections launched alone, no faster inside the PDL-chained stack)
-    const double e8 = 0.0;
     const int64_t G = L->G, T8 = L->tiles8, T4 = L->tiles4;
     double best = 1e30;
     for (int S4 = 1; S4 <= 8; S4 *= 2) {
@@ -203,7 +202,7 @@ void best_split(mq_layer_s* L, int kind) {
             const int64_t grid = std::min<int64_t>(units, L->num_sms);
             // wide tiles: split items only when every slice runs in one round (the together-mode join)
             if (kind > 0 && S8 > 1 && units > L->num_sms) continue;
-            const double c8 = (k8 * double(G) + e8) / S8 + kUnitCost + (S8 > 1 ? kSplitCost : 0.0);
+            const double c8 = k8 * double(G) / S8 + kUnitCost + (S8 > 1 ? kSplitCost : 0.0);
             const double c4 = double(G) / S4 + kUnitCost + (S4 > 1 ? kSplitCost : 0.0);
             double span = 0;
             for (int64_t b = 0; b < grid; ++b) {  // CTA b runs units b, b + grid, ...
